@@ -1,0 +1,129 @@
+/*
+ * pdl.h -- C ABI of libpdl.so, the B200 (sm_100a) implementation of the hot
+ * path of PolyDL (arXiv 2006.02230) as exposed by the reference `looprank`
+ * package.  Plain pointers and sizes only; every tensor pointer is a
+ * caller-owned DEVICE pointer, every call is stream-ordered and asynchronous,
+ * no call allocates device memory.  Return 0 on success, a negative PDL_E*
+ * code otherwise; pdl_last_error() gives a thread-local message.
+ *
+ * What each entry point replaces in the reference (/root/reference):
+ *
+ *   pdl_conv2d_fwd_nchw16c  -- simcache.interpret (pkg/src/looprank/simcache.py:89-204)
+ *       executing the Fig. 9 blocked convolution nest
+ *       whose innermost band is the `#pragma microkernel gemm(...)` region
+ *       (loopdsl.py:250, 502-514; substitute_microkernel loopdsl.py:747-760).
+ *       Layouts are the nest's array declarations: input nChw16c, filter
+ *       KCRS16c16k, output nKhw16k.  Unlike the .pdl nest (which cannot express
+ *       padding), x is UNPADDED and the kernel zero-fills the
+ *       halo; pad = R/2 in every BASELINE config.
+ *   pdl_conv2d_fwd_prepacked / pdl_conv2d_prepack_weights -- the same call
+ *       split in two: a one-time weight reorder (+ hi/lo TF32 split for 3xTF32)
+ *       and the per-batch convolution.  This mirrors how the paper's CPU
+ *       implementation keeps KCRS16c16k weights in a blocked format prepared
+ *       once per layer.
+ *   PDL_BIAS | PDL_RELU flags -- the conv -> bias+ReLU program (two nests in
+ *       one .pdl Program) fused per Alg. 3 (
+ *       SPEC.md:531-591): the element-wise op is applied to the fully reduced
+ *       accumulator before the single store.
+ *   pdl_gemm_f32            -- interpret on the Fig. 1 / Fig. 12 GEMM nest
+ *       C[i][j] += A[i][k]*B[k][j] in its
+ *       beta*C + alpha*A*B form, row-major.
+ *   pdl_bias_relu_nchw16c   -- the stand-alone element-wise nest
+ *       `output = max(output + bias, 0.0)` (the unfused GPU baseline).
+ *
+ * Numerics: PDL_MODE_3XTF32 (default) splits every fp32 operand x into
+ * hi = tf32(x) and lo = x - hi and accumulates hi*hi + hi*lo + lo*hi in fp32
+ * on the tcgen05 tensor cores (max-rel <= 1e-5 vs the float64 oracle);
+ * PDL_MODE_TF32 is one tensor pass (<= 1e-2); PDL_MODE_FP32 runs exact fp32
+ * FMAs on the CUDA cores (also the path for shapes TMA cannot describe).
+ */
+#ifndef PDL_H_
+#define PDL_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDL_ABI_VERSION 1
+
+/* Schedule knobs chosen by the ranker (paper_2006_02230_b200/rank.py);
+ * NULL or zero fields = library default.  bm is fixed at 128 (tcgen05 M). */
+typedef struct pdl_tile_cfg {
+    int bm;        /* output rows (pixels / GEMM M) per CTA tile: 128          */
+    int bn;        /* output columns (K channels / GEMM N) per tile: 64|128|256 */
+    int bk;        /* reduction elements per pipeline stage (16*cg for conv)    */
+    int stages;    /* smem pipeline depth                                       */
+    int cluster_m; /* reserved (1)                                              */
+    int cluster_n; /* reserved (1)                                              */
+    int split_k;   /* reserved (1)                                              */
+    int raster;    /* 0: M-tiles fastest, 1: N-tiles fastest                    */
+} pdl_tile_cfg;
+
+enum {
+    PDL_BIAS = 1,             /* y += bias[k]                                  */
+    PDL_RELU = 2,             /* y = max(y, 0)   (after bias)                  */
+    PDL_MODE_3XTF32 = 0 << 4, /* default                                       */
+    PDL_MODE_TF32 = 1 << 4,
+    PDL_MODE_FP32 = 2 << 4,
+    PDL_MODE_MASK = 3 << 4
+};
+
+enum {
+    PDL_OK = 0,
+    PDL_EINVAL = -1,     /* bad shape / argument                                */
+    PDL_EALIGN = -2,     /* pointer or stride not 16-byte aligned               */
+    PDL_EDEVICE = -3,    /* no sm_100 device                                    */
+    PDL_ELAUNCH = -4,    /* CUDA launch / driver failure                        */
+    PDL_EWORKSPACE = -5, /* workspace missing or too small                      */
+    PDL_EUNSUPPORTED = -6
+};
+
+enum { PDL_OP_CONV2D = 1, PDL_OP_GEMM = 2 };
+
+/* Convolution, raw KCRS16c16k weights.  Needs a workspace of
+ * pdl_workspace_bytes(PDL_OP_CONV2D, dims, cfg) bytes (the prepacked weights),
+ * dims = {N, C, K, H, W, R, S, stride, pad, flags}. */
+int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, float *y,
+                           int N, int C, int K, int H, int W, int R, int S, int stride,
+                           int pad, unsigned flags, const pdl_tile_cfg *cfg, void *workspace,
+                           size_t ws_bytes, void *stream);
+
+/* One-time weight reorder KCRS16c16k -> tensor-core operand image (and hi/lo
+ * split for 3xTF32).  `packed` must hold pdl_conv2d_packed_bytes(...) bytes. */
+size_t pdl_conv2d_packed_bytes(int C, int K, int R, int S, unsigned flags);
+int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R, int S,
+                               unsigned flags, void *stream);
+int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *bias,
+                             float *y, int N, int C, int K, int H, int W, int R, int S,
+                             int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg,
+                             void *stream);
+
+/* C = alpha * A B + beta * C, row-major with leading dimensions lda/ldb/ldc. */
+int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda,
+                 int ldb, int ldc, float alpha, float beta, unsigned flags,
+                 const pdl_tile_cfg *cfg, void *workspace, size_t ws_bytes, void *stream);
+
+/* Unfused element-wise pass over y[N][K/16][P][Q][16] (the GPU baseline). */
+int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int Q,
+                          unsigned flags, void *stream);
+
+size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg);
+
+/* Tile config the library would pick for a conv / GEMM (for the ranker and
+ * the bench's roofline report).  Writes *cfg, returns 0. */
+int pdl_default_cfg(int op, const int *dims, pdl_tile_cfg *cfg);
+
+/* Number of kernel launches the last successful call on this thread issued. */
+int pdl_last_launch_count(void);
+
+const char *pdl_last_error(void);
+int pdl_abi_version(void);
+/* 0 if the current device is sm_100 (B200), PDL_EDEVICE otherwise. */
+int pdl_device_check(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDL_H_ */

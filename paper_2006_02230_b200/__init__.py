@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) implementation of the PolyDL (arXiv 2006.02230) hot path:
+fp32 blocked convolution (nChw16c / KCRS16c16k), row-major fp32 GEMM and the
+fused conv + bias + ReLU operator, behind the reference `looprank` package's
+loop-nest entry points (see loopdsl.py / executor.py) and ranking API.
+
+Kernels live in libpdl.so (csrc/, C ABI in include/pdl.h); there is no CPU
+fallback on this path.
+"""
+from ._lib import PdlDeviceError, PdlError, PdlShapeError, TileCfg  # noqa: F401
+from .ops import (PackedWeights, bias_relu_, conv2d_nchw16c, conv_out_hw,  # noqa: F401
+                  device_ok, gemm, prepack_weights)
+
+__version__ = "0.1.0"

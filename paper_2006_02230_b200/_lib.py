@@ -1,0 +1,136 @@
+"""ctypes binding of libpdl.so (include/pdl.h).
+
+The product path has no CPU fallback: if the library is missing or the device
+is not an sm_100 B200, every op raises `PdlError` / `PdlDeviceError`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpdl.so")
+
+PDL_BIAS = 1
+PDL_RELU = 2
+PDL_MODE_3XTF32 = 0 << 4
+PDL_MODE_TF32 = 1 << 4
+PDL_MODE_FP32 = 2 << 4
+PDL_MODE_MASK = 3 << 4
+PDL_OP_CONV2D = 1
+PDL_OP_GEMM = 2
+
+MODES = {"3xtf32": PDL_MODE_3XTF32, "tf32": PDL_MODE_TF32, "fp32": PDL_MODE_FP32}
+
+PDL_OK, PDL_EINVAL, PDL_EALIGN, PDL_EDEVICE, PDL_ELAUNCH, PDL_EWORKSPACE, PDL_EUNSUPPORTED = (
+    0, -1, -2, -3, -4, -5, -6)
+
+# Symbols include/pdl.h declares (checked by tests/test_capi.py without a GPU).
+EXPORTS = (
+    "pdl_conv2d_fwd_nchw16c", "pdl_conv2d_packed_bytes", "pdl_conv2d_prepack_weights",
+    "pdl_conv2d_fwd_prepacked", "pdl_gemm_f32", "pdl_bias_relu_nchw16c",
+    "pdl_workspace_bytes", "pdl_default_cfg", "pdl_last_launch_count", "pdl_last_error",
+    "pdl_abi_version", "pdl_device_check",
+)
+
+
+class PdlError(RuntimeError):
+    """A libpdl call returned a nonzero status (message from pdl_last_error)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[{code}] {message}")
+        self.code = code
+
+
+class PdlDeviceError(PdlError):
+    pass
+
+
+class PdlShapeError(PdlError, ValueError):
+    pass
+
+
+class TileCfg(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in
+                ("bm", "bn", "bk", "stages", "cluster_m", "cluster_n", "split_k", "raster")]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+    @classmethod
+    def make(cls, **kw) -> "TileCfg":
+        c = cls()
+        for k, v in kw.items():
+            setattr(c, k, int(v))
+        return c
+
+
+_lock = threading.Lock()
+_lib = None
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_u = ctypes.c_uint
+_sz = ctypes.c_size_t
+
+
+def _declare(L):
+    L.pdl_conv2d_fwd_nchw16c.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
+        _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
+    L.pdl_conv2d_packed_bytes.argtypes = [_i, _i, _i, _i, _u]
+    L.pdl_conv2d_packed_bytes.restype = _sz
+    L.pdl_conv2d_prepack_weights.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
+    L.pdl_conv2d_fwd_prepacked.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
+        _u, ctypes.POINTER(TileCfg), _vp]
+    L.pdl_gemm_f32.argtypes = [_vp, _vp, _vp] + [_i] * 6 + [
+        ctypes.c_float, ctypes.c_float, _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
+    L.pdl_bias_relu_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
+    L.pdl_workspace_bytes.argtypes = [_i, ctypes.POINTER(_i), ctypes.POINTER(TileCfg)]
+    L.pdl_workspace_bytes.restype = _sz
+    L.pdl_default_cfg.argtypes = [_i, ctypes.POINTER(_i), ctypes.POINTER(TileCfg)]
+    L.pdl_last_launch_count.argtypes = []
+    L.pdl_last_error.argtypes = []
+    L.pdl_last_error.restype = ctypes.c_char_p
+    L.pdl_abi_version.argtypes = []
+    L.pdl_device_check.argtypes = []
+    for name in EXPORTS:
+        if name not in ("pdl_conv2d_packed_bytes", "pdl_workspace_bytes", "pdl_last_error"):
+            getattr(L, name).restype = _i
+
+
+def lib():
+    """Load libpdl.so once; raise if it was not built (no silent fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise PdlError(PDL_EDEVICE, f"{LIB_PATH} is missing: run "
+                                   "`python -c 'import __graft_entry__ as g; g.build()'`")
+                L = ctypes.CDLL(LIB_PATH)
+                _declare(L)
+                _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == PDL_OK:
+        return
+    msg = lib().pdl_last_error().decode(errors="replace")
+    if rc == PDL_EDEVICE:
+        raise PdlDeviceError(rc, msg)
+    if rc in (PDL_EINVAL, PDL_EALIGN, PDL_EUNSUPPORTED, PDL_EWORKSPACE):
+        raise PdlShapeError(rc, msg)
+    raise PdlError(rc, msg)
+
+
+def default_cfg(op: int, dims) -> TileCfg:
+    arr = (_i * len(dims))(*[int(d) for d in dims])
+    c = TileCfg()
+    check(lib().pdl_default_cfg(op, arr, ctypes.byref(c)))
+    return c
+
+
+def last_launch_count() -> int:
+    return int(lib().pdl_last_launch_count())

@@ -1,0 +1,439 @@
+// pdl_capi.cu -- the extern "C" boundary of libpdl.so (include/pdl.h): argument
+// validation, tile-config selection, TMA tensor-map encoding and kernel launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pdl.h"
+#include "pdl_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PDL_ELAUNCH, "%s: %s", what, cudaGetErrorString(e));
+    return PDL_OK;
+}
+
+// ---------------------------------------------------------------- driver entry
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int get_encode() {
+    std::call_once(g_encode_once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+    });
+    if (!g_encode) return fail(PDL_EDEVICE, "cuTensorMapEncodeTiled unavailable");
+    return PDL_OK;
+}
+
+int encode(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
+           const cuuint64_t *strides_bytes, const cuuint32_t *box, CUtensorMapSwizzle sw,
+           const char *what) {
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void *>(base),
+                          dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PDL_EINVAL, "tensor map encode failed (%s, rc=%d)", what, (int)r);
+    return PDL_OK;
+}
+
+// ---------------------------------------------------------------- device check
+int g_dev_ok = -1;
+std::once_flag g_dev_once;
+int sm_count = 148;
+
+int device_check() {
+    std::call_once(g_dev_once, [] {
+        int dev = 0, major = 0, minor = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) { g_dev_ok = 0; return; }
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+        g_dev_ok = (major == 10 && minor == 0) ? 1 : 0;
+    });
+    if (g_dev_ok != 1) return fail(PDL_EDEVICE, "libpdl requires an sm_100 (B200) device");
+    return PDL_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------- launch helpers
+template <int KIND, int BN, int CG, bool SPLIT3>
+int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid, cudaStream_t s) {
+    using L = pdl::Smem<KIND, BN, CG, SPLIT3>;
+    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    });
+    if (attr_err != cudaSuccess)
+        return fail(PDL_ELAUNCH, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+    kern<<<grid, 256, L::TOTAL, s>>>(maps, p);
+    ++g_launches;
+    return check_launch("tile_mma_kernel");
+}
+
+template <int KIND, bool SPLIT3>
+int dispatch_tile(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid,
+                  cudaStream_t s) {
+    if constexpr (KIND == pdl::KIND_GEMM) {
+        switch (bn) {
+            case 64: return launch_tile<KIND, 64, 1, SPLIT3>(maps, p, grid, s);
+            case 128: return launch_tile<KIND, 128, 1, SPLIT3>(maps, p, grid, s);
+            case 256: return launch_tile<KIND, 256, 1, SPLIT3>(maps, p, grid, s);
+        }
+    } else {
+        if (bn == 64 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3>(maps, p, grid, s);
+        if (bn == 64 && cg == 2) return launch_tile<KIND, 64, 2, SPLIT3>(maps, p, grid, s);
+        if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3>(maps, p, grid, s);
+        if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3>(maps, p, grid, s);
+        if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3>(maps, p, grid, s);
+        if (bn == 256 && cg == 1) return launch_tile<KIND, 256, 1, SPLIT3>(maps, p, grid, s);
+    }
+    return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d", bn, cg);
+}
+
+// ---------------------------------------------------------------- conv geometry
+struct ConvGeom {
+    int P, Q;        // true output extents
+    int Hg, Wg;      // geometry extents (flattened for 1x1/s1/p0)
+    int Pg, Qg;
+    bool flat;
+    int BW, BH, BNI, tiles_w, tiles_h, tiles_n;
+};
+
+ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad) {
+    ConvGeom g{};
+    g.P = (H + 2 * pad - R) / stride + 1;
+    g.Q = (W + 2 * pad - S) / stride + 1;
+    g.flat = (R == 1 && S == 1 && stride == 1 && pad == 0);
+    g.Hg = g.flat ? 1 : H;
+    g.Wg = g.flat ? H * W : W;
+    g.Pg = g.flat ? 1 : g.P;
+    g.Qg = g.flat ? g.P * g.Q : g.Q;
+    g.BW = std::min(g.Qg, 128);
+    g.BH = std::min(g.Pg, 128 / g.BW);
+    g.BNI = (g.BH == g.Pg) ? std::max(1, std::min(N, 128 / (g.BW * g.BH))) : 1;
+    g.tiles_w = (g.Qg + g.BW - 1) / g.BW;
+    g.tiles_h = (g.Pg + g.BH - 1) / g.BH;
+    g.tiles_n = (N + g.BNI - 1) / g.BNI;
+    return g;
+}
+
+void conv_default_cfg(int C, int K, pdl_tile_cfg *c) {
+    const int CT = C / 16;
+    c->bm = 128;
+    c->bn = K >= 128 ? 128 : 64;
+    int cg = (CT % 2 == 0) ? 2 : 1;
+    c->bk = 16 * cg;
+    c->stages = 0;
+    c->cluster_m = c->cluster_n = c->split_k = 1;
+    c->raster = 0;
+}
+
+int conv_check(const float *x, const float *y, int N, int C, int K, int H, int W, int R, int S,
+               int stride, int pad) {
+    if (N <= 0 || C <= 0 || K <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0)
+        return fail(PDL_EINVAL, "conv: non-positive dimension");
+    if (C % 16 || K % 16) return fail(PDL_EINVAL, "conv: C and K must be multiples of 16 (got %d, %d)", C, K);
+    if (stride != 1 && stride != 2) return fail(PDL_EUNSUPPORTED, "conv: stride must be 1 or 2");
+    if (pad < 0 || pad >= R || pad >= S) return fail(PDL_EINVAL, "conv: bad padding %d", pad);
+    if ((H + 2 * pad - R) < 0 || (W + 2 * pad - S) < 0) return fail(PDL_EINVAL, "conv: empty output");
+    if (!aligned16(x) || !aligned16(y)) return fail(PDL_EALIGN, "conv: x / y must be 16-byte aligned");
+    return PDL_OK;
+}
+
+int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, int N, int C, int K,
+                int H, int W, int R, int S, int stride, int pad, unsigned flags,
+                const pdl_tile_cfg *cfg_in, cudaStream_t st) {
+    int rc;
+    if ((rc = get_encode())) return rc;
+    const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
+    pdl_tile_cfg cfg;
+    conv_default_cfg(C, K, &cfg);
+    if (cfg_in) {
+        if (cfg_in->bn) cfg.bn = cfg_in->bn;
+        if (cfg_in->bk) cfg.bk = cfg_in->bk;
+        cfg.raster = cfg_in->raster;
+    }
+    const int CT = C / 16, KT = K / 16, cg = cfg.bk / 16;
+    if (cg < 1 || CT % cg) return fail(PDL_EINVAL, "conv: bk=%d does not divide C=%d", cfg.bk, C);
+    if (K % cfg.bn && cfg.bn > K) cfg.bn = 64;
+    const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad);
+    if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
+
+    pdl::TmaMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    const cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
+    if (stride == 1) {
+        const cuuint64_t dims[5] = {16, (cuuint64_t)g.Wg, (cuuint64_t)g.Hg, (cuuint64_t)CT, (cuuint64_t)N};
+        const cuuint64_t str[4] = {64, (cuuint64_t)g.Wg * 64, (cuuint64_t)g.Hg * g.Wg * 64,
+                                   (cuuint64_t)CT * g.Hg * g.Wg * 64};
+        if ((rc = encode(&maps.a[0], x, 5, dims, str, abox, CU_TENSOR_MAP_SWIZZLE_64B, "conv x")))
+            return rc;
+    } else {
+        for (int ph = 0; ph < 2; ++ph)
+            for (int pw = 0; pw < 2; ++pw) {
+                const cuuint64_t dims[5] = {16, (cuuint64_t)((W - pw + 1) / 2),
+                                            (cuuint64_t)((H - ph + 1) / 2), (cuuint64_t)CT,
+                                            (cuuint64_t)N};
+                const cuuint64_t str[4] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 64,
+                                           (cuuint64_t)CT * H * W * 64};
+                const float *base = x + ((size_t)ph * W + pw) * 16;
+                if ((rc = encode(&maps.a[ph * 2 + pw], base, 5, dims, str, abox,
+                                 CU_TENSOR_MAP_SWIZZLE_64B, "conv x parity")))
+                    return rc;
+            }
+    }
+    {
+        const int planes = split ? 2 : 1;
+        const cuuint64_t dims[5] = {16, (cuuint64_t)K, (cuuint64_t)(R * S), (cuuint64_t)CT, (cuuint64_t)planes};
+        const cuuint64_t str[4] = {64, (cuuint64_t)K * 64, (cuuint64_t)R * S * K * 64,
+                                   (cuuint64_t)CT * R * S * K * 64};
+        const cuuint32_t bbox[5] = {16, (cuuint32_t)cfg.bn, 1, (cuuint32_t)cg, (cuuint32_t)planes};
+        if ((rc = encode(&maps.b, wp, 5, dims, str, bbox, CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
+            return rc;
+    }
+    pdl::TileParams p{};
+    p.num_kb = (CT / cg) * R * S;
+    p.n_out = K;
+    p.flags = flags;
+    p.bias = bias;
+    p.out = y;
+    p.nimg = N;
+    p.P = g.Pg;
+    p.Q = g.Qg;
+    p.KT = KT;
+    p.R = R;
+    p.S = S;
+    p.pad = pad;
+    p.stride = stride;
+    p.CT = CT;
+    p.BW = g.BW;
+    p.BH = g.BH;
+    p.BNI = g.BNI;
+    p.tiles_w = g.tiles_w;
+    p.tiles_h = g.tiles_h;
+    p.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
+    p.raster = cfg.raster;
+    const int n_tiles = (K + cfg.bn - 1) / cfg.bn;
+    dim3 grid = cfg.raster ? dim3(n_tiles, p.m_tiles) : dim3(p.m_tiles, n_tiles);
+    if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, maps, p, grid, st);
+    return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, maps, p, grid, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int pdl_abi_version(void) { return PDL_ABI_VERSION; }
+const char *pdl_last_error(void) { return g_err.c_str(); }
+int pdl_last_launch_count(void) { return g_launches; }
+int pdl_device_check(void) { return device_check(); }
+
+size_t pdl_conv2d_packed_bytes(int C, int K, int R, int S, unsigned flags) {
+    const int planes = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 ? 2 : 1;
+    return (size_t)planes * C * K * R * S * sizeof(float);
+}
+
+int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R, int S,
+                               unsigned flags, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if (C % 16 || K % 16 || R <= 0 || S <= 0) return fail(PDL_EINVAL, "prepack: bad shape");
+    if (!aligned16(w) || !aligned16(packed)) return fail(PDL_EALIGN, "prepack: unaligned pointer");
+    const int split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
+    const long long total = (long long)K * C * R * S;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    pdl::prepack_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        w, reinterpret_cast<float *>(packed), C / 16, K / 16, R * S, split);
+    ++g_launches;
+    return check_launch("prepack_weights_kernel");
+}
+
+int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *bias, float *y,
+                             int N, int C, int K, int H, int W, int R, int S, int stride, int pad,
+                             unsigned flags, const pdl_tile_cfg *cfg, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
+    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
+        return fail(PDL_EUNSUPPORTED, "conv: PDL_MODE_FP32 takes raw weights (pdl_conv2d_fwd_nchw16c)");
+    if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
+    return conv_fwd_tc(x, reinterpret_cast<const float *>(packed_w), bias, y, N, C, K, H, W, R, S,
+                       stride, pad, flags, cfg, (cudaStream_t)stream);
+}
+
+int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, float *y, int N,
+                           int C, int K, int H, int W, int R, int S, int stride, int pad,
+                           unsigned flags, const pdl_tile_cfg *cfg, void *workspace,
+                           size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
+    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32) {
+        const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+        const long long total = (long long)N * (K / 16) * P * Q;
+        pdl::simt_conv_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
+            x, w, bias, y, N, C / 16, K / 16, H, W, R, S, stride, pad, P, Q, flags);
+        ++g_launches;
+        return check_launch("simt_conv_kernel");
+    }
+    const size_t need = pdl_conv2d_packed_bytes(C, K, R, S, flags);
+    if (!workspace || ws_bytes < need)
+        return fail(PDL_EWORKSPACE, "conv: workspace of %zu bytes required", need);
+    if ((rc = pdl_conv2d_prepack_weights(w, workspace, C, K, R, S, flags, stream))) return rc;
+    rc = conv_fwd_tc(x, reinterpret_cast<const float *>(workspace), bias, y, N, C, K, H, W, R, S,
+                     stride, pad, flags, cfg, st);
+    if (rc == PDL_OK) g_launches = 2;
+    return rc;
+}
+
+int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda, int ldb,
+                 int ldc, float alpha, float beta, unsigned flags, const pdl_tile_cfg *cfg_in,
+                 void *workspace, size_t ws_bytes, void *stream) {
+    (void)workspace;
+    (void)ws_bytes;
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if (M < 0 || N < 0 || K < 0) return fail(PDL_EINVAL, "gemm: negative dimension");
+    if (lda < std::max(K, 1) || ldb < std::max(N, 1) || ldc < std::max(N, 1))
+        return fail(PDL_EINVAL, "gemm: leading dimension too small");
+    if (M == 0 || N == 0) return PDL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned mode = flags & PDL_MODE_MASK;
+    const bool tma_ok = K > 0 && aligned16(A) && aligned16(B) && aligned16(C) && lda % 4 == 0 &&
+                        ldb % 4 == 0 && ldc % 4 == 0 && N % 4 == 0 &&
+                        (!(flags & PDL_BIAS) || (cfg_in == nullptr || true));
+    if (mode == PDL_MODE_FP32 || !tma_ok) {
+        dim3 grid((N + 63) / 64, (M + 63) / 64);
+        pdl::simt_gemm_kernel<<<grid, 256, 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc, alpha, beta,
+                                                    nullptr, flags & ~(unsigned)PDL_BIAS);
+        ++g_launches;
+        return check_launch("simt_gemm_kernel");
+    }
+    if ((rc = get_encode())) return rc;
+    int bn = N <= 64 ? 64 : 128;
+    int raster = 0;
+    if (cfg_in) {
+        if (cfg_in->bn) bn = cfg_in->bn;
+        raster = cfg_in->raster;
+    }
+    pdl::TmaMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+        const cuuint64_t str[1] = {(cuuint64_t)lda * 4};
+        const cuuint32_t box[2] = {32, 128};
+        if ((rc = encode(&maps.a[0], A, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B, "gemm A"))) return rc;
+    }
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)K};
+        const cuuint64_t str[1] = {(cuuint64_t)ldb * 4};
+        const cuuint32_t box[2] = {32, 32};
+        if ((rc = encode(&maps.b, B, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, "gemm B"))) return rc;
+    }
+    pdl::TileParams p{};
+    p.num_kb = (K + 31) / 32;
+    p.n_out = N;
+    p.flags = flags & ~(unsigned)PDL_BIAS;
+    p.bias = nullptr;
+    p.out = C;
+    p.M = M;
+    p.ldc = ldc;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.raster = raster;
+    const int m_tiles = (M + 127) / 128, n_tiles = (N + bn - 1) / bn;
+    p.m_tiles = m_tiles;
+    dim3 grid = raster ? dim3(n_tiles, m_tiles) : dim3(m_tiles, n_tiles);
+    if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, maps, p, grid, st);
+    return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, maps, p, grid, st);
+}
+
+int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int Q, unsigned flags,
+                          void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if (K % 16 || N < 0 || P < 0 || Q < 0) return fail(PDL_EINVAL, "bias_relu: bad shape");
+    if (!aligned16(y) || ((flags & PDL_BIAS) && (!bias || !aligned16(bias))))
+        return fail(PDL_EALIGN, "bias_relu: unaligned pointer");
+    const long long n4 = (long long)N * K * P * Q / 4;
+    if (n4 == 0) return PDL_OK;
+    const int blocks = (int)std::min<long long>((n4 + 255) / 256, 148LL * 8);
+    pdl::bias_relu_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<float4 *>(y), reinterpret_cast<const float4 *>(bias), n4, P * Q, K / 16, flags);
+    ++g_launches;
+    return check_launch("bias_relu_kernel");
+}
+
+size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg) {
+    (void)cfg;
+    if (op == PDL_OP_CONV2D && dims) {
+        // dims = {N, C, K, H, W, R, S, stride, pad, flags}
+        return pdl_conv2d_packed_bytes(dims[1], dims[2], dims[5], dims[6], (unsigned)dims[9]);
+    }
+    return 0;
+}
+
+int pdl_default_cfg(int op, const int *dims, pdl_tile_cfg *cfg) {
+    if (!cfg || !dims) return fail(PDL_EINVAL, "default_cfg: null argument");
+    if (op == PDL_OP_CONV2D) {
+        conv_default_cfg(dims[1], dims[2], cfg);
+        return PDL_OK;
+    }
+    if (op == PDL_OP_GEMM) {
+        // dims = {M, N, K}
+        cfg->bm = 128;
+        cfg->bn = dims[1] <= 64 ? 64 : 128;
+        cfg->bk = 32;
+        cfg->stages = 0;
+        cfg->cluster_m = cfg->cluster_n = cfg->split_k = 1;
+        cfg->raster = 0;
+        return PDL_OK;
+    }
+    return fail(PDL_EINVAL, "default_cfg: unknown op %d", op);
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""Torch-facing ops over the C ABI.  torch supplies device memory and the
+current CUDA stream; all arithmetic runs in libpdl.so kernels.
+
+Layouts (the reference nest's array declarations):
+  x  [N][C/16][H][W][16]          nChw16c activations, UNPADDED
+  w  [K/16][C/16][R][S][16c][16k]  KCRS16c16k weights
+  y  [N][K/16][P][Q][16]           nKhw16k outputs
+  bias [K]
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import (PDL_BIAS, PDL_RELU, MODES, TileCfg, check, lib)
+
+
+def _mode(mode: str) -> int:
+    try:
+        return MODES[mode.lower()]
+    except KeyError:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {sorted(MODES)}") from None
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need_cuda_f32(name, t):
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _cfg_ptr(cfg):
+    if cfg is None:
+        return None
+    if isinstance(cfg, dict):
+        cfg = TileCfg.make(**cfg)
+    return ctypes.byref(cfg)
+
+
+def conv_out_hw(h, w, r, s, stride, pad):
+    return (h + 2 * pad - r) // stride + 1, (w + 2 * pad - s) // stride + 1
+
+
+@dataclass
+class PackedWeights:
+    """Tensor-core operand image of KCRS16c16k weights (hi/lo planes for 3xTF32)."""
+    data: torch.Tensor
+    C: int
+    K: int
+    R: int
+    S: int
+    mode: str
+
+
+def prepack_weights(w: torch.Tensor, mode: str = "3xtf32", stream=None) -> PackedWeights:
+    _need_cuda_f32("w", w)
+    kt, ct, r, s, c16, k16 = w.shape
+    assert c16 == 16 and k16 == 16, "weights must be KCRS16c16k"
+    C, K = ct * 16, kt * 16
+    flags = _mode(mode)
+    nbytes = lib().pdl_conv2d_packed_bytes(C, K, r, s, flags)
+    out = torch.empty(nbytes // 4, dtype=torch.float32, device=w.device)
+    check(lib().pdl_conv2d_prepack_weights(_ptr(w), _ptr(out), C, K, r, s, flags,
+                                           ctypes.c_void_p(_stream(stream))))
+    return PackedWeights(out, C, K, r, s, mode.lower())
+
+
+def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride: int = 1,
+                   pad: int = 0, relu: bool = False, mode: str = "3xtf32", cfg=None,
+                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Blocked conv fwd (+bias, +ReLU fused in the epilogue).  `w` is either raw
+    KCRS16c16k weights or a PackedWeights from prepack_weights()."""
+    _need_cuda_f32("x", x)
+    _need_cuda_f32("bias", bias)
+    n, ct, h, wd, v = x.shape
+    if v != 16:
+        raise ValueError("x must be nChw16c")
+    packed = w if isinstance(w, PackedWeights) else None
+    if packed is not None:
+        C, K, R, S = packed.C, packed.K, packed.R, packed.S
+        if packed.mode != mode.lower():
+            raise ValueError(f"weights packed for {packed.mode}, called with {mode}")
+    else:
+        _need_cuda_f32("w", w)
+        kt, ct2, R, S, _, _ = w.shape
+        C, K = ct2 * 16, kt * 16
+    if C != ct * 16:
+        raise ValueError(f"channel mismatch: x has {ct * 16}, w has {C}")
+    P, Q = conv_out_hw(h, wd, R, S, stride, pad)
+    y = out if out is not None else torch.empty((n, K // 16, P, Q, 16), dtype=torch.float32,
+                                                device=x.device)
+    _need_cuda_f32("out", y)
+    flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    st = ctypes.c_void_p(_stream(stream))
+    if packed is not None:
+        check(lib().pdl_conv2d_fwd_prepacked(_ptr(x), _ptr(packed.data), _ptr(bias), _ptr(y), n, C,
+                                             K, h, wd, R, S, stride, pad, flags, _cfg_ptr(cfg), st))
+    else:
+        nbytes = lib().pdl_conv2d_packed_bytes(C, K, R, S, flags)
+        ws = torch.empty(max(nbytes // 4, 4), dtype=torch.float32, device=x.device)
+        check(lib().pdl_conv2d_fwd_nchw16c(_ptr(x), _ptr(w), _ptr(bias), _ptr(y), n, C, K, h, wd,
+                                           R, S, stride, pad, flags, _cfg_ptr(cfg), _ptr(ws),
+                                           nbytes, st))
+    return y
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha: float = 1.0,
+         beta: float = 0.0, relu: bool = False, mode: str = "3xtf32", cfg=None,
+         stream=None) -> torch.Tensor:
+    """C = alpha * A @ B + beta * C (row-major fp32)."""
+    for nm, t in (("a", a), ("b", b)):
+        _need_cuda_f32(nm, t)
+    m, k = a.shape
+    k2, n = b.shape
+    if k != k2:
+        raise ValueError(f"inner dimensions differ: {k} vs {k2}")
+    if c is None:
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs c")
+        c = torch.empty((m, n), dtype=torch.float32, device=a.device)
+    _need_cuda_f32("c", c)
+    flags = _mode(mode) | (PDL_RELU if relu else 0)
+    check(lib().pdl_gemm_f32(_ptr(a), _ptr(b), _ptr(c), m, n, k, k, n, n, float(alpha),
+                             float(beta), flags, _cfg_ptr(cfg), None, 0,
+                             ctypes.c_void_p(_stream(stream))))
+    return c
+
+
+def bias_relu_(y: torch.Tensor, bias: torch.Tensor | None, relu: bool = True,
+               stream=None) -> torch.Tensor:
+    """Unfused element-wise pass y = max(y + bias, 0) in place (GPU baseline)."""
+    _need_cuda_f32("y", y)
+    _need_cuda_f32("bias", bias)
+    n, kt, p, q, v = y.shape
+    flags = (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    check(lib().pdl_bias_relu_nchw16c(_ptr(y), _ptr(bias), n, kt * 16, p, q, flags,
+                                      ctypes.c_void_p(_stream(stream))))
+    return y
+
+
+def device_ok() -> bool:
+    return lib().pdl_device_check() == 0
+
+
+__all__ = ["conv2d_nchw16c", "prepack_weights", "PackedWeights", "gemm", "bias_relu_",
+           "device_ok", "conv_out_hw", "TileCfg"]
+_ = _lib
