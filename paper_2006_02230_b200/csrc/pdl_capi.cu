@@ -85,6 +85,9 @@ int device_check() {
     return PDL_OK;
 }
 
+// Reduction elements accumulated in TMEM before an fp32 round-to-nearest drain.
+constexpr int kSegElems = 256;
+
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ---------------------------------------------------------------- launch helpers
@@ -227,6 +230,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     }
     pdl::TileParams p{};
     p.num_kb = (CT / cg) * R * S;
+    p.seg_kb = std::max(1, kSegElems / (16 * cg));
     p.n_out = K;
     p.flags = flags;
     p.bias = bias;
@@ -375,6 +379,7 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     }
     pdl::TileParams p{};
     p.num_kb = (K + 31) / 32;
+    p.seg_kb = kSegElems / 32;
     p.n_out = N;
     p.flags = flags & ~(unsigned)PDL_BIAS;
     p.bias = nullptr;

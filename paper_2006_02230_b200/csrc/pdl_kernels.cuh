@@ -45,6 +45,7 @@ struct TileParams {
     int tiles_w, tiles_h;  // tile grid over (Q, P); images fastest-after
     int m_tiles;           // number of M tiles
     int raster;            // 0: blockIdx.x -> M tile, 1: -> N tile
+    int seg_kb;            // k-blocks per TMEM accumulation segment
 };
 
 struct TmaMaps {
@@ -76,7 +77,7 @@ struct Smem {
     static constexpr int B_HI = SPLIT3 ? 2 * G::A_BYTES : G::A_BYTES;
     static constexpr int B_LO = B_HI + G::B_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE;
-    static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
+    static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + alignment slack
     static_assert(STAGES >= 2, "tile too large for a 2-stage pipeline");
 };
 
@@ -106,26 +107,74 @@ __device__ __forceinline__ void split_tile(uint8_t *hi, uint8_t *lo, int bytes, 
     }
 }
 
+// Epilogue for 16 consecutive output columns [col0, col0+16) of one row.
+template <int KIND>
+__device__ __forceinline__ void store16(const TileParams &p, float *dst, int col0,
+                                        const float *v) {
+    const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
+    const bool relu = p.flags & PDL_RELU;
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+        const int col = col0 + q4 * 4;
+        if (KIND == KIND_GEMM && col >= p.n_out) break;
+        float4 r = make_float4(v[q4 * 4 + 0], v[q4 * 4 + 1], v[q4 * 4 + 2], v[q4 * 4 + 3]);
+        if (KIND == KIND_GEMM) {
+            r.x *= p.alpha; r.y *= p.alpha; r.z *= p.alpha; r.w *= p.alpha;
+            if (p.beta != 0.f) {
+                const float4 c = *reinterpret_cast<const float4 *>(dst + q4 * 4);
+                r.x += p.beta * c.x; r.y += p.beta * c.y;
+                r.z += p.beta * c.z; r.w += p.beta * c.w;
+            }
+        }
+        if (has_bias) {
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col));
+            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+        }
+        if (relu) {  // Python max(v, 0.0): keep v unless 0 > v
+            r.x = (0.f > r.x) ? 0.f : r.x;
+            r.y = (0.f > r.y) ? 0.f : r.y;
+            r.z = (0.f > r.z) ? 0.f : r.z;
+            r.w = (0.f > r.w) ? 0.f : r.w;
+        }
+        *reinterpret_cast<float4 *>(dst + q4 * 4) = r;
+    }
+}
+
+// Implicit-GEMM tile engine.  One CTA = one 128 x BN output tile.
+//   warp 0      TMA producer (one lane)
+//   warp 1      tcgen05.mma issuer (one lane)
+//   warp 2      TMEM allocator
+//   warps 4-7   3xTF32 split of each landed stage, then TMEM drain + epilogue
+// The reduction is cut into segments of p.seg_kb k-blocks; each segment is
+// accumulated in one of two TMEM buffers (ping-pong) and drained into fp32
+// registers with round-to-nearest adds.  The tensor core's accumulator
+// truncates, so an unsegmented K=4096 sum drifts to ~3e-5 relative error;
+// 256-element segments keep it near 3e-6 at any K.
 template <int KIND, int BN, int CG, bool SPLIT3>
 __global__ void __launch_bounds__(256, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
     using G = Geo<KIND, BN, CG>;
     using L = Smem<KIND, BN, CG, SPLIT3>;
     constexpr int STAGES = L::STAGES;
+    constexpr bool SEGMENTED = BN <= 128;  // register budget for the running sums
+    constexpr uint32_t TMEM_COLS = SEGMENTED ? 2 * BN : BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem =
         reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);
     uint64_t *ready = full + STAGES;
     uint64_t *empty = ready + STAGES;
-    uint64_t *tmem_full = empty + STAGES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    uint64_t *tmem_full = empty + STAGES;  // [2]
+    uint64_t *tmem_empty = tmem_full + 2;  // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int m_tile = p.raster ? blockIdx.y : blockIdx.x;
     const int n_tile = p.raster ? blockIdx.x : blockIdx.y;
     const int n0 = n_tile * BN;
+    const int seg_kb = SEGMENTED ? p.seg_kb : p.num_kb;
+    const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&maps.b);
@@ -135,10 +184,13 @@ __global__ void __launch_bounds__(256, 1)
             mbar_init(&ready[s], 128);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmem_full[b], 1);
+            mbar_init(&tmem_empty[b], 128);
+        }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<BN>(tmem_slot);
+    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -209,7 +261,14 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t smem0 = smem_u32(smem);
             int s = 0;
             uint32_t ph = 0;
+            int g = 0, in_seg = 0;
+            uint32_t d_tmem = tmem_base;
             for (int kb = 0; kb < p.num_kb; ++kb) {
+                if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
+                    mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    d_tmem = tmem_base + (SEGMENTED ? (uint32_t)((g & 1) * BN) : 0u);
+                }
                 mbar_wait(SPLIT3 ? &ready[s] : &full[s], ph);
                 tc_fence_after();
                 const uint32_t st = smem0 + s * L::STAGE;
@@ -218,8 +277,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                     for (int kk = 0; kk < G::KK; ++kk) {
                         const uint32_t a_off = c * G::A_SUB + kk * 32;
-                        uint64_t ahi = smem_desc(st + L::A_HI + a_off, 16, a_sbo, layout);
-                        uint64_t alo = smem_desc(st + L::A_LO + a_off, 16, a_sbo, layout);
+                        const uint64_t ahi = smem_desc(st + L::A_HI + a_off, 16, a_sbo, layout);
+                        const uint64_t alo = smem_desc(st + L::A_LO + a_off, 16, a_sbo, layout);
                         uint64_t bhi, blo;
                         if (KIND == KIND_GEMM) {
                             // MN-major tf32 operand: 128B rows of 32 n-values, 32B-atom
@@ -232,52 +291,81 @@ __global__ void __launch_bounds__(256, 1)
                             bhi = smem_desc(st + L::B_HI + b_off, 16, 512, LAYOUT_SW64);
                             blo = smem_desc(st + L::B_LO + b_off, 16, 512, LAYOUT_SW64);
                         }
-                        const uint32_t acc = (kb | c | kk) != 0;
-                        mma_tf32(tmem_base, ahi, bhi, idesc, acc);
+                        const uint32_t acc = (in_seg | c | kk) != 0;
+                        mma_tf32(d_tmem, ahi, bhi, idesc, acc);
                         if (SPLIT3) {
-                            mma_tf32(tmem_base, ahi, blo, idesc, 1);
-                            mma_tf32(tmem_base, alo, bhi, idesc, 1);
+                            mma_tf32(d_tmem, ahi, blo, idesc, 1);
+                            mma_tf32(d_tmem, alo, bhi, idesc, 1);
                         }
                     }
                 }
                 mma_commit(&empty[s]);
                 if (++s == STAGES) { s = 0; ph ^= 1; }
+                if (++in_seg == seg_kb || kb + 1 == p.num_kb) {
+                    mma_commit(&tmem_full[g & 1]);
+                    in_seg = 0;
+                    ++g;
+                }
             }
-            mma_commit(tmem_full);
         }
     } else if (warp >= 4) {
         const int tid = threadIdx.x - 128;
-        // ===================== 3xTF32 split =====================
-        if (SPLIT3) {
-            const int a_valid = KIND == KIND_GEMM ? G::A_SUB : 64 * p.BW * p.BH * p.BNI;
+        const int quarter = warp - 4;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        float sum[SEGMENTED ? BN : 1];
+        if (SEGMENTED) {
+#pragma unroll
+            for (int i = 0; i < (SEGMENTED ? BN : 1); ++i) sum[i] = 0.f;
+        }
+        int drained = 0;
+        auto drain = [&](int g) {
+            mbar_wait(&tmem_full[g & 1], (g >> 1) & 1);
+            tc_fence_after();
+            if (SEGMENTED) {
+                const uint32_t base = tmem_base + lane_off + (uint32_t)((g & 1) * BN);
+#pragma unroll
+                for (int j = 0; j < BN / 16; ++j) {
+                    float v[16];
+                    tmem_ld16(base + j * 16, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) sum[(SEGMENTED ? j * 16 + i : 0)] += v[i];
+                }
+                tc_fence_before();
+                mbar_arrive(&tmem_empty[g & 1]);
+            }
+        };
+        const int a_valid = KIND == KIND_GEMM ? G::A_SUB : 64 * p.BW * p.BH * p.BNI;
+        {
             int s = 0;
             uint32_t ph = 0;
             for (int kb = 0; kb < p.num_kb; ++kb) {
-                mbar_wait(&full[s], ph);
-                uint8_t *st = smem + s * L::STAGE;
+                if (SPLIT3) {
+                    // ===================== 3xTF32 split =====================
+                    mbar_wait(&full[s], ph);
+                    uint8_t *st = smem + s * L::STAGE;
 #pragma unroll
-                for (int c = 0; c < G::NSUB; ++c)
-                    split_tile(st + L::A_HI + c * G::A_SUB, st + L::A_LO + c * G::A_SUB,
-                               a_valid, tid, 128);
-                if (KIND == KIND_GEMM) split_tile(st + L::B_HI, st + L::B_LO, G::B_BYTES, tid, 128);
-                fence_proxy_async_smem();
-                mbar_arrive(&ready[s]);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
+                    for (int c = 0; c < G::NSUB; ++c)
+                        split_tile(st + L::A_HI + c * G::A_SUB, st + L::A_LO + c * G::A_SUB,
+                                   a_valid, tid, 128);
+                    if (KIND == KIND_GEMM)
+                        split_tile(st + L::B_HI, st + L::B_LO, G::B_BYTES, tid, 128);
+                    fence_proxy_async_smem();
+                    mbar_arrive(&ready[s]);
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+                // drain segments that finished at least one k-block ago
+                if (SEGMENTED && drained < nseg - 1 && kb >= (drained + 1) * seg_kb) drain(drained++);
             }
         }
-        // ===================== epilogue: TMEM -> regs -> global =====================
-        const int quarter = warp - 4;
-        const int row = quarter * 32 + lane;
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
+        // ===================== epilogue =====================
         bool valid;
         float *obase = nullptr;
-        size_t cstride = 0;  // bytes between consecutive 16-col chunks (in floats)
+        size_t cstride = 0;
         if (KIND == KIND_GEMM) {
             const int gm = m0 + row;
             valid = gm < p.M;
             obase = p.out + (size_t)(valid ? gm : 0) * p.ldc;
-            cstride = 16;
         } else {
             const int per_img = p.BW * p.BH;
             const int il = row / per_img;
@@ -291,44 +379,28 @@ __global__ void __launch_bounds__(256, 1)
                     ((size_t)(valid ? pp : 0) * p.Q + (valid ? qq : 0)) * 16;
             cstride = plane;  // next 16-channel block kt
         }
-        const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
-        const bool relu = p.flags & PDL_RELU;
-#pragma unroll 1
-        for (int j = 0; j < BN / 16; ++j) {
-            float v[16];
-            tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + j * 16, v);
-            const int col0 = n0 + j * 16;
-            if (!valid || col0 >= p.n_out) continue;
-            float *dst;
-            if (KIND == KIND_GEMM) {
-                dst = obase + col0;
-            } else {
-                dst = obase + (size_t)(col0 >> 4) * cstride;
-            }
+        if (SEGMENTED) {
+            while (drained < nseg) drain(drained++);
+            if (valid) {
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                const int col = col0 + q4 * 4;
-                if (KIND == KIND_GEMM && col >= p.n_out) break;
-                float4 r = make_float4(v[q4 * 4 + 0], v[q4 * 4 + 1], v[q4 * 4 + 2], v[q4 * 4 + 3]);
-                if (KIND == KIND_GEMM) {
-                    r.x *= p.alpha; r.y *= p.alpha; r.z *= p.alpha; r.w *= p.alpha;
-                    if (p.beta != 0.f) {
-                        const float4 c = *reinterpret_cast<const float4 *>(dst + q4 * 4);
-                        r.x += p.beta * c.x; r.y += p.beta * c.y;
-                        r.z += p.beta * c.z; r.w += p.beta * c.w;
+                for (int j = 0; j < BN / 16; ++j) {
+                    const int col0 = n0 + j * 16;
+                    if (col0 < p.n_out) {
+                        float *dst = KIND == KIND_GEMM ? obase + col0 : obase + (size_t)(col0 >> 4) * cstride;
+                        store16<KIND>(p, dst, col0, &sum[SEGMENTED ? j * 16 : 0]);
                     }
                 }
-                if (has_bias) {
-                    const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col));
-                    r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
-                }
-                if (relu) {
-                    r.x = (0.f > r.x) ? 0.f : r.x;
-                    r.y = (0.f > r.y) ? 0.f : r.y;
-                    r.z = (0.f > r.z) ? 0.f : r.z;
-                    r.w = (0.f > r.w) ? 0.f : r.w;
-                }
-                *reinterpret_cast<float4 *>(dst + q4 * 4) = r;
+            }
+        } else {
+            drain(0);
+#pragma unroll 1
+            for (int j = 0; j < BN / 16; ++j) {
+                float v[16];
+                tmem_ld16(tmem_base + lane_off + j * 16, v);
+                const int col0 = n0 + j * 16;
+                if (!valid || col0 >= p.n_out) continue;
+                float *dst = KIND == KIND_GEMM ? obase + col0 : obase + (size_t)(col0 >> 4) * cstride;
+                store16<KIND>(p, dst, col0, v);
             }
         }
     }
@@ -337,7 +409,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<BN>(tmem_base);
+        tmem_dealloc<TMEM_COLS>(tmem_base);
     }
 }
 
