@@ -1,0 +1,576 @@
+#!/usr/bin/env python
+"""bench.py -- B200 benchmark of the PolyDL hot path (driver contract).
+
+Default workload (BASELINE.json configs[3]/[4]): one "step" = one forward pass
+of the 20 distinct ResNet-50 v1 conv layers, each a FUSED conv + bias + ReLU in
+3xTF32 (fp32-accurate), nChw16c / KCRS16c16k, on a global minibatch of 256
+images sharded contiguously across the ranks (256/G per GPU, no collective on
+the path; weights replicated once with an NCCL broadcast before timing).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload suite|gemm|pr1] [--mode 3xtf32|tf32] [--unfused]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "conv/GEMM GFLOP/s per layer and % of B200 roofline at 1/2/4/8 GPUs vs CPU oracle"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "gemm", "pr1"])
+    ap.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--batch", type=int, default=256, help="global minibatch (suite)")
+    ap.add_argument("--unfused", action="store_true", help="also time conv + separate bias/ReLU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
+    return ap.parse_args()
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            m = json.load(f)
+        peaks.update(hbm_gbs=float(m["hbm_gbs"]), bf16_tflops=float(m["bf16_tflops"]),
+                     bf16_tflops_sustained=float(m.get("bf16_tflops_sustained", m["bf16_tflops"])),
+                     source="MEASURED_PEAKS.json")
+    t = os.path.join(ROOT, "profiles", "peaks_tf32.json")
+    if os.path.exists(t):
+        with open(t) as f:
+            m = json.load(f)
+        peaks["tf32_tflops"] = float(m["tf32_tflops"])
+        peaks["tf32_source"] = "profiles/peaks_tf32.json (cuBLAS TF32 8192^3, measured on B200)"
+    else:
+        peaks["tf32_tflops"] = peaks["bf16_tflops"] / 2
+        peaks["tf32_source"] = "bf16 measured / 2 (planning estimate)"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s, p in zip(sm, power) if p > 200] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ----------------------------------------------------------------------------- helpers
+def ncu_traffic(kernel_tag: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        s = json.load(f)
+    ent = s.get("kernels", {}).get(kernel_tag)
+    return None if ent is None else ent.get("dram_bytes")
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_prepare(layers):
+    import oracle
+    from paper_2006_02230_b200 import workloads as W
+    prepared = []
+    for layer in layers:
+        x, w, b = W.conv_inputs(layer, 1, seed=900 + layer.idx)
+        xp = oracle.pad_nchw16c(x, layer.R, layer.S, layer.stride, layer.pad)
+        y = np.empty((1, layer.K // 16, layer.P, layer.Q, 16), np.float32)
+        prepared.append((layer, xp, np.ascontiguousarray(w), b, y))
+    return prepared
+
+
+def cpu_step(prepared, threads):
+    import oracle
+    for layer, xp, w, b, y in prepared:
+        oracle.cpu_conv2d_f32(xp, w, b, layer.stride, layer.P, layer.Q, relu=True,
+                              threads=threads, out=y)
+
+
+def cpu_suite_sample(layers, seconds_budget: float, threads: int):
+    """Time the oracle's fp32 Fig. 9 port (kind "port") on 1 image per layer,
+    repeated up to the time budget.  Returns (GFLOP/s, reps, seconds)."""
+    prepared = cpu_prepare(layers)
+    flops = sum(l.flops(1) for l in layers)
+    cpu_step(prepared, threads)  # page-in
+    t_total, reps = 0.0, 0
+    while reps == 0 or (t_total < seconds_budget and reps < 50):
+        t0 = time.perf_counter()
+        cpu_step(prepared, threads)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    return flops * reps / t_total / 1e9, reps, t_total
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_suite(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    import paper_2006_02230_b200 as P
+    from paper_2006_02230_b200 import _lib, workloads as W
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if not P.device_ok():
+        raise SystemExit("libpdl.so: no sm_100 device")
+    if args.batch % world:
+        raise SystemExit(f"--batch {args.batch} not divisible by {world} ranks")
+    n_local = args.batch // world
+    layers = W.LAYERS
+    peaks = load_peaks()
+    mode_peak = peaks["tf32_tflops"] * 1e12 / (3.0 if args.mode == "3xtf32" else 1.0)
+
+    # ---- data: inputs seeded per (layer, rank); weights from rank 0, broadcast once
+    bufs = []
+    for layer in layers:
+        ca = layer.C_alloc
+        g = torch.Generator(device=dev)
+        g.manual_seed(10_000 * layer.idx + rank)
+        x = torch.rand((n_local, ca // 16, layer.H, layer.W, 16), generator=g, device=dev) * 2 - 1
+        gw = torch.Generator(device=dev)
+        gw.manual_seed(7 + layer.idx)
+        w = torch.rand((layer.K // 16, ca // 16, layer.R, layer.S, 16, 16), generator=gw,
+                       device=dev) * 2 - 1
+        b = torch.rand((layer.K,), generator=gw, device=dev) - 0.5
+        if layer.C != ca:
+            x[..., layer.C:] = 0
+            w[:, :, :, :, layer.C:, :] = 0
+        if world > 1:
+            dist.broadcast(w, 0)
+            dist.broadcast(b, 0)
+        pw = P.prepack_weights(w, mode=args.mode)
+        y = torch.empty((n_local, layer.K // 16, layer.P, layer.Q, 16), device=dev)
+        bufs.append((layer, x, w, b, pw, y))
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    launches_per_step = 0
+
+    def step(ev=None):
+        nonlocal launches_per_step
+        cnt = 0
+        for i, (layer, x, w, b, pw, y) in enumerate(bufs):
+            if ev is not None:
+                ev[i][0].record(stream)
+            P.conv2d_nchw16c(x, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
+                             mode=args.mode, out=y)
+            cnt += _lib.last_launch_count()
+            if ev is not None:
+                ev[i][1].record(stream)
+        launches_per_step = cnt
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, max over ranks)
+    clocks = ClockSampler(local)
+    ev_layers = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in bufs] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)  # let the sampler attach before load starts
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(ev_layers[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_flops = sum(l.flops(args.batch) for l in layers)
+    value = total_flops / (ms_step / 1e3) / 1e9
+
+    # ---- per-layer breakdown (this rank's device events)
+    per_layer = []
+    for i, (layer, *_rest) in enumerate(bufs):
+        lms = sum(ev_layers[k][i][0].elapsed_time(ev_layers[k][i][1]) for k in range(args.steps)) / args.steps
+        rf = W.Roofline(layer.flops(n_local), layer.bytes(n_local, bias=True), mode_peak,
+                        peaks["hbm_gbs"] * 1e9)
+        per_layer.append({"layer": layer.name(), "ms": round(lms, 4),
+                          "gflops": round(layer.flops(n_local) / (lms / 1e3) / 1e9, 1),
+                          "bound": rf.bound, "roofline_frac": round(rf.fraction(lms / 1e3), 3),
+                          "share": None})
+    tot_layer_ms = sum(d["ms"] for d in per_layer)
+    for d in per_layer:
+        d["share"] = round(d["ms"] / tot_layer_ms, 3)
+
+    # ---- dominant kernel roofline (contract object)
+    dom_i = max(range(len(per_layer)), key=lambda i: per_layer[i]["ms"])
+    dom_layer = bufs[dom_i][0]
+    dom_s = per_layer[dom_i]["ms"] / 1e3
+    rf = W.Roofline(dom_layer.flops(n_local), dom_layer.bytes(n_local, bias=True), mode_peak,
+                    peaks["hbm_gbs"] * 1e9)
+    if rf.bound == "tensor":
+        achieved = dom_layer.flops(n_local) / dom_s / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
+                "peak_source": peaks["source"] + " bf16 dense",
+                "mode_peak": round(mode_peak / 1e12, 1),
+                "mode_peak_source": f"{peaks['tf32_source']}" + (" / 3 (3xTF32 = 3 tensor passes)" if args.mode == "3xtf32" else ""),
+                "frac_of_mode_peak": round(achieved / (mode_peak / 1e12), 4)}
+    else:
+        achieved = dom_layer.bytes(n_local, bias=True) / dom_s / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "peak_source": peaks["source"]}
+    roof.update(kernel=f"tile_mma_kernel[{dom_layer.name()}]",
+                algorithmic_per_launch={"flops": dom_layer.flops(n_local),
+                                        "bytes": dom_layer.bytes(n_local, bias=True)},
+                avg_launch_ms=round(dom_s * 1e3, 4), traffic=ncu_traffic(dom_layer.name()))
+
+    out = {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded U[-1,1) activations/weights, U[-0.5,0.5) bias; ResNet-50 "
+                   "v1 shapes only, no dataset or checkpoint)",
+           "config": {"workload": "resnet50_v1_20_distinct_layers_fused_conv_bias_relu",
+                      "global_batch": args.batch, "per_gpu_batch": n_local, "mode": args.mode,
+                      "layout": "nChw16c x / KCRS16c16k w (prepacked once) / nKhw16k y",
+                      "parallelism": f"batch-sharded x{world}, no collective",
+                      "l2": "step working set %.1f GB >> 126 MB L2; each layer's inputs were "
+                            "last touched one full step earlier" % (
+                                sum(l.bytes(n_local) for l in layers) / 1e9),
+                      "flops_per_step": total_flops},
+           "roofline": roof, "clocks": clk, "gpu_launches": launches_per_step * args.steps,
+           "layers": per_layer}
+
+    # ---- e2e through the public API with host buffers
+    if not args.no_e2e:
+        out["e2e"] = run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream)
+
+    # ---- unfused GPU baseline comparison (optional)
+    if args.unfused:
+        out["unfused"] = run_unfused(args, bufs, P, torch, stream)
+
+    # ---- CPU baseline on rank 0, N=1 only
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gf, reps, secs = cpu_suite_sample(layers, args.cpu_seconds, cpu_cores())
+        out["cpu_baseline"] = {"value": round(gf, 2), "unit": "GFLOP/s", "cores": cpu_cores(),
+                               "kind": "port",
+                               "sample": f"oracle fp32 Fig.9 loop nest (oracle/pdl_oracle.c), "
+                                         f"1 image per layer x 20 layers, fused bias+ReLU, "
+                                         f"{reps} reps in {secs:.1f} s"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream):
+    """Same metric through the public API with pinned HOST buffers: each step
+    copies every layer's x host->device, runs the fused conv, and copies y back."""
+    hx = [torch.empty(x.shape, dtype=torch.float32, pin_memory=True) for (_, x, *_r) in bufs]
+    hy = [torch.empty(y.shape, dtype=torch.float32, pin_memory=True) for (*_r, y) in bufs]
+    for h, (_, x, *_r) in zip(hx, bufs):
+        h.copy_(x)
+    h2d = sum(h.numel() * 4 for h in hx)
+    d2h = sum(h.numel() * 4 for h in hy)
+
+    def step():
+        for (layer, x, w, b, pw, y), xh, yh in zip(bufs, hx, hy):
+            x.copy_(xh, non_blocking=True)
+            P.conv2d_nchw16c(x, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
+                             mode=args.mode, out=y)
+            yh.copy_(y, non_blocking=True)
+
+    steps = max(1, min(args.steps, 3))
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(total_flops / (ms / steps / 1e3) / 1e9, 1), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "ms_per_step": round(ms / steps, 3),
+            "path": "paper_2006_02230_b200.conv2d_nchw16c -> libpdl.so pdl_conv2d_fwd_prepacked, "
+                    "pinned host x/y, copies inside the timed region"}
+
+
+def run_unfused(args, bufs, P, torch, stream):
+    res = []
+    for layer, x, w, b, pw, y in bufs:
+        def fused():
+            P.conv2d_nchw16c(x, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
+                             mode=args.mode, out=y)
+
+        def unfused():
+            P.conv2d_nchw16c(x, pw, None, stride=layer.stride, pad=layer.pad, mode=args.mode, out=y)
+            P.bias_relu_(y, b)
+
+        t = {}
+        for name, fn in (("fused", fused), ("unfused", unfused)):
+            for _ in range(2):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t[name] = e0.elapsed_time(e1) / 5
+        n = x.shape[0]
+        res.append({"layer": layer.name(), "fused_ms": round(t["fused"], 4),
+                    "unfused_ms": round(t["unfused"], 4),
+                    "speedup": round(t["unfused"] / t["fused"], 3),
+                    "hbm_bytes_saved": layer.unfused_extra_bytes(n)})
+    return res
+
+
+# ----------------------------------------------------------------------------- GEMM / PR1
+def run_gemm(args, rank, world, local):
+    import torch
+    import paper_2006_02230_b200 as P
+    from paper_2006_02230_b200 import workloads as W
+    torch.cuda.set_device(local)
+    peaks = load_peaks()
+    mode_peak = peaks["tf32_tflops"] * 1e12 / (3.0 if args.mode == "3xtf32" else 1.0)
+    stream = torch.cuda.current_stream()
+    rows, tot_f, tot_ms = [], 0.0, 0.0
+    for (m, n, k) in W.GEMM_SWEEP:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(m * 31 + n * 7 + k)
+        # rotate 4 input sets so consecutive launches do not hit in L2 for small shapes
+        sets = [(torch.rand((m, k), generator=g, device="cuda") * 2 - 1,
+                 torch.rand((k, n), generator=g, device="cuda") * 2 - 1,
+                 torch.empty((m, n), device="cuda")) for _ in range(4)]
+        flush = torch.empty(64 * 1024 * 1024, device="cuda")  # 256 MB > L2
+        for i in range(args.warmup):
+            a, b, c = sets[i % 4]
+            P.gemm(a, b, c, mode=args.mode)
+        ms = 0.0
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda._sleep(200_000)  # GPU busy while the host enqueues the launch
+            a, b, c = sets[i % 4]
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            P.gemm(a, b, c, mode=args.mode)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        ms /= args.steps
+        f = W.gemm_flops(m, n, k)
+        rf = W.Roofline(f, W.gemm_bytes(m, n, k), mode_peak, peaks["hbm_gbs"] * 1e9)
+        rows.append({"shape": [m, n, k], "ms": round(ms, 4), "gflops": round(f / ms / 1e6, 1),
+                     "bound": rf.bound, "roofline_frac": round(rf.fraction(ms / 1e3), 3)})
+        tot_f += f
+        tot_ms += ms
+    big = max(rows, key=lambda r: r["ms"])
+    m, n, k = big["shape"]
+    achieved = W.gemm_flops(m, n, k) / (big["ms"] / 1e3) / 1e12
+    return {"metric": METRIC, "value": round(tot_f / tot_ms / 1e6, 1), "unit": "GFLOP/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tot_ms, 4), "higher_is_better": True, "scaling": "replicas only",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic U[-1,1)",
+            "config": {"workload": "gemm_sweep_rowmajor_fp32", "mode": args.mode,
+                       "l2": "256 MB flush between timed launches"},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 2),
+                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": round(achieved / peaks["bf16_tflops"], 4),
+                         "mode_peak": round(mode_peak / 1e12, 1),
+                         "frac_of_mode_peak": round(achieved * 1e12 / mode_peak, 4),
+                         "kernel": f"tile_mma_kernel[gemm {m}x{n}x{k}]", "traffic": None},
+            "gemms": rows, "gpu_launches": len(rows) * args.steps}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The reference's CPU implementation of the path = the oracle port of the
+    Fig. 9 loop nest (the reference itself is a Python interpreter that cannot
+    travel to the box).  Rank 0 only."""
+    if rank != 0:
+        return None
+    from paper_2006_02230_b200 import workloads as W
+    cores = cpu_cores()
+    layers = W.LAYERS
+    flops = sum(l.flops(1) for l in layers)
+    prepared = cpu_prepare(layers)
+    for _ in range(args.warmup):
+        cpu_step(prepared, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_step(prepared, cores)
+    secs = time.perf_counter() - t0
+    value = flops * args.steps / secs / 1e9
+    sample = ("oracle fp32 Fig.9 loop nest, 1 image per layer x 20 ResNet-50 layers, fused "
+              "bias+ReLU, per step")
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(secs / args.steps * 1e3, 2), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded U[-1,1))",
+            "config": {"workload": "resnet50_v1_20_distinct_layers_fused_conv_bias_relu",
+                       "global_batch": args.batch, "mode": "fp32 (CPU)",
+                       "sample_per_step": "1 image per layer"},
+            "cpu_baseline": {"value": round(value, 2), "unit": "GFLOP/s", "cores": cores,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_info()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    elif args.workload == "suite":
+        out = run_suite(args, rank, world, local)
+    elif args.workload == "gemm":
+        out = run_gemm(args, rank, world, local) if rank == 0 else None
+    else:
+        args.batch = 1
+        out = run_suite_pr1(args, rank, world, local) if rank == 0 else None
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def run_suite_pr1(args, rank, world, local):
+    """PR1 (configs[0]): N=1, C=K=64, 56x56, 3x3, s1, p1, no bias."""
+    import torch
+    import paper_2006_02230_b200 as P
+    from paper_2006_02230_b200 import workloads as W
+    torch.cuda.set_device(local)
+    peaks = load_peaks()
+    mode_peak = peaks["tf32_tflops"] * 1e12 / (3.0 if args.mode == "3xtf32" else 1.0)
+    layer = W.PR1
+    x, w, _ = W.conv_inputs(layer, 1, seed=1234, bias=False)
+    xs = [torch.from_numpy(x).cuda() for _ in range(8)]
+    pw = P.prepack_weights(torch.from_numpy(w).cuda(), mode=args.mode)
+    y = torch.empty((1, 4, 56, 56, 16), device="cuda")
+    for i in range(args.warmup):
+        P.conv2d_nchw16c(xs[i % 8], pw, stride=1, pad=1, mode=args.mode, out=y)
+    flush = torch.empty(64 * 1024 * 1024, device="cuda")
+    stream = torch.cuda.current_stream()
+    ms = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda._sleep(200_000)  # GPU busy while the host enqueues the launch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.conv2d_nchw16c(xs[i % 8], pw, stride=1, pad=1, mode=args.mode, out=y)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    ms /= args.steps
+    f = layer.flops(1)
+    rf = W.Roofline(f, layer.bytes(1), mode_peak, peaks["hbm_gbs"] * 1e9)
+    return {"metric": METRIC, "value": round(f / ms / 1e6, 1), "unit": "GFLOP/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic U[-1,1) seed 1234",
+            "config": {"workload": "PR1 conv 3x3 N=1 C=K=64 56x56", "mode": args.mode,
+                       "l2": "256 MB flush between timed launches"},
+            "roofline": {"bound": rf.bound, "frac_of_mode_peak": round(rf.fraction(ms / 1e3), 4)},
+            "gpu_launches": args.steps}
+
+
+if __name__ == "__main__":
+    main()

@@ -161,7 +161,10 @@ int pdl_oracle_gemm_f64(const float *A, const float *B, const float *C0, double 
 /* ---------------- timed fp32 CPU baseline (kind "port") ---------------- */
 
 /* Fig. 9 over a PRE-PADDED input (the paper's layout assumption), fp32,
- * microkernel outer-product order, OpenMP over (img, ofm_tile). */
+ * microkernel outer-product order, OpenMP over (img, ofm_tile, oj): the
+ * paper parallelises img; at small batch the ofm_tile and
+ * output-row loops are added so every host core has work (stated in
+ * DESIGN.md).  Per-element reduction order is unchanged (ct, kj, ki, ifm). */
 int pdl_cpu_conv2d_f32(const float *xp, const float *w, const float *bias, float *y,
                        int N, int C, int K, int Hp, int Wp, int R, int S, int stride,
                        int P, int Q, int relu, int threads) {
@@ -169,19 +172,18 @@ int pdl_cpu_conv2d_f32(const float *xp, const float *w, const float *bias, float
     int CT = C / V, KT = K / V;
 #ifdef _OPENMP
     if (threads > 0) omp_set_num_threads(threads);
-#pragma omp parallel for collapse(2) schedule(static)
+#pragma omp parallel for collapse(3) schedule(static)
 #endif
     for (int img = 0; img < N; img++)
-        for (int kt = 0; kt < KT; kt++) {
-            float *yb = y + ((size_t)img * KT + kt) * P * Q * V;
-            memset(yb, 0, (size_t)P * Q * V * sizeof(float));
-            for (int ct = 0; ct < CT; ct++)
-                for (int oj = 0; oj < P; oj++)
+        for (int kt = 0; kt < KT; kt++)
+            for (int oj = 0; oj < P; oj++) {
+                float *yr = y + (((size_t)img * KT + kt) * P + oj) * Q * V;
+                memset(yr, 0, (size_t)Q * V * sizeof(float));
+                for (int ct = 0; ct < CT; ct++)
                     for (int kj = 0; kj < R; kj++)
                         for (int ki = 0; ki < S; ki++) {
                             const float *wb = w + ((((size_t)kt * CT + ct) * R + kj) * S + ki) * V * V;
                             const float *xr = xp + (((size_t)img * CT + ct) * Hp + oj * stride + kj) * Wp * V;
-                            float *yr = yb + (size_t)oj * Q * V;
                             for (int oi = 0; oi < Q; oi++) {
                                 const float *xi = xr + (size_t)(oi * stride + ki) * V;
                                 float acc[V];
@@ -193,14 +195,14 @@ int pdl_cpu_conv2d_f32(const float *xp, const float *w, const float *bias, float
                                 for (int v = 0; v < V; v++) yr[oi * V + v] = acc[v];
                             }
                         }
-            if (relu || bias) {
-                for (int pq = 0; pq < P * Q; pq++)
-                    for (int v = 0; v < V; v++) {
-                        float t = yb[(size_t)pq * V + v] + (bias ? bias[kt * V + v] : 0.f);
-                        yb[(size_t)pq * V + v] = (relu && t < 0.f) ? 0.f : t;
-                    }
+                if (relu || bias) {
+                    for (int q = 0; q < Q; q++)
+                        for (int v = 0; v < V; v++) {
+                            float t = yr[(size_t)q * V + v] + (bias ? bias[kt * V + v] : 0.f);
+                            yr[(size_t)q * V + v] = (relu && t < 0.f) ? 0.f : t;
+                        }
+                }
             }
-        }
     return 0;
 }
 
