@@ -1,0 +1,67 @@
+"""CPU-only checks of the C ABI boundary: the library loads, exports every
+symbol include/pdl.h declares, and reports a clean error without a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2006_02230_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "pdl.h")).read()
+    return sorted(set(re.findall(r"\b(pdl_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_built():
+    assert os.path.exists(_lib.LIB_PATH), "run __graft_entry__.build() first"
+
+
+def test_exports_match_header():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+
+
+def test_abi_version_and_cfg():
+    L = _lib.lib()
+    assert L.pdl_abi_version() == 1
+    cfg = _lib.default_cfg(_lib.PDL_OP_CONV2D, [28, 64, 64, 56, 56, 3, 3, 1, 1, 0])
+    assert cfg.bm == 128 and cfg.bn == 64 and cfg.bk in (16, 32)
+    cfg = _lib.default_cfg(_lib.PDL_OP_GEMM, [4096, 4096, 4096])
+    assert cfg.bn in (64, 128, 256)
+
+
+def test_workspace_and_packed_bytes():
+    L = _lib.lib()
+    assert L.pdl_conv2d_packed_bytes(64, 128, 3, 3, _lib.PDL_MODE_3XTF32) == 2 * 64 * 128 * 9 * 4
+    assert L.pdl_conv2d_packed_bytes(64, 128, 3, 3, _lib.PDL_MODE_TF32) == 64 * 128 * 9 * 4
+    dims = (ctypes.c_int * 10)(2, 64, 128, 14, 14, 3, 3, 1, 1, 0)
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 64 * 128 * 9 * 4
+
+
+def test_no_gpu_is_a_loud_error():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    L = _lib.lib()
+    assert L.pdl_device_check() == _lib.PDL_EDEVICE
+    assert b"sm_100" in L.pdl_last_error()
+    with pytest.raises(_lib.PdlError):
+        _lib.check(L.pdl_gemm_f32(None, None, None, 4, 4, 4, 4, 4, 4, 1.0, 0.0, 0, None, None,
+                                  0, None))
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2006_02230_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
