@@ -226,7 +226,7 @@ def run_suite(args, rank, world, local):
         if world > 1:
             dist.broadcast(w, 0)
             dist.broadcast(b, 0)
-        pw = P.prepack_weights(w, mode=args.mode)
+        pw = P.prepack_weights(w, mode=args.mode, channels=layer.C)
         y = torch.empty((n_local, layer.K // 16, layer.P, layer.Q, 16), device=dev)
         bufs.append((layer, x, w, b, pw, y))
     torch.cuda.synchronize()

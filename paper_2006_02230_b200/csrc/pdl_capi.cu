@@ -102,7 +102,7 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid, c
     });
     if (attr_err != cudaSuccess)
         return fail(PDL_ELAUNCH, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-    kern<<<grid, 256, L::TOTAL, s>>>(maps, p);
+    kern<<<grid, pdl::kThreads, L::TOTAL, s>>>(maps, p);
     ++g_launches;
     return check_launch("tile_mma_kernel");
 }
@@ -110,11 +110,10 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid, c
 template <int KIND, bool SPLIT3>
 int dispatch_tile(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid,
                   cudaStream_t s) {
-    if constexpr (KIND == pdl::KIND_GEMM) {
+    if constexpr (KIND == pdl::KIND_GEMM || KIND == pdl::KIND_STEM) {
         switch (bn) {
             case 64: return launch_tile<KIND, 64, 1, SPLIT3>(maps, p, grid, s);
             case 128: return launch_tile<KIND, 128, 1, SPLIT3>(maps, p, grid, s);
-            case 256: return launch_tile<KIND, 256, 1, SPLIT3>(maps, p, grid, s);
         }
     } else {
         if (bn == 64 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3>(maps, p, grid, s);
@@ -122,7 +121,6 @@ int dispatch_tile(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParam
         if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3>(maps, p, grid, s);
         if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3>(maps, p, grid, s);
         if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3>(maps, p, grid, s);
-        if (bn == 256 && cg == 1) return launch_tile<KIND, 256, 1, SPLIT3>(maps, p, grid, s);
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d", bn, cg);
 }
@@ -154,8 +152,13 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad) {
     return g;
 }
 
+// Narrow-channel path (ResNet stem): <= 4 real input channels, <= 8 taps per row.
+bool is_stem(int C, int S, int stride) { return C <= 4 && S <= 8 && (stride == 1 || stride == 2); }
+
+int ceil16(int c) { return (c + 15) / 16; }
+
 void conv_default_cfg(int C, int K, pdl_tile_cfg *c) {
-    const int CT = C / 16;
+    const int CT = ceil16(C);
     c->bm = 128;
     c->bn = K >= 128 ? 128 : 64;
     int cg = (CT % 2 == 0) ? 2 : 1;
@@ -169,7 +172,7 @@ int conv_check(const float *x, const float *y, int N, int C, int K, int H, int W
                int stride, int pad) {
     if (N <= 0 || C <= 0 || K <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0)
         return fail(PDL_EINVAL, "conv: non-positive dimension");
-    if (C % 16 || K % 16) return fail(PDL_EINVAL, "conv: C and K must be multiples of 16 (got %d, %d)", C, K);
+    if (K % 16) return fail(PDL_EINVAL, "conv: K must be a multiple of 16 (got %d)", K);
     if (stride != 1 && stride != 2) return fail(PDL_EUNSUPPORTED, "conv: stride must be 1 or 2");
     if (pad < 0 || pad >= R || pad >= S) return fail(PDL_EINVAL, "conv: bad padding %d", pad);
     if ((H + 2 * pad - R) < 0 || (W + 2 * pad - S) < 0) return fail(PDL_EINVAL, "conv: empty output");
@@ -177,11 +180,70 @@ int conv_check(const float *x, const float *y, int N, int C, int K, int H, int W
     return PDL_OK;
 }
 
+int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, int N, int C,
+                  int K, int H, int W, int R, int S, int stride, int pad, unsigned flags,
+                  const pdl_tile_cfg *cfg_in, cudaStream_t st) {
+    int rc;
+    const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
+    const int bn = (cfg_in && cfg_in->bn) ? cfg_in->bn : (K % 128 == 0 ? 128 : 64);
+    const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+    const int BW = std::min({Q, 128, (256 - S) / stride + 1});
+    const int box_w = (BW - 1) * stride + S;
+    pdl::TmaMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    {
+        const cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
+        const cuuint64_t str[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
+        const cuuint32_t box[5] = {4, (cuuint32_t)box_w, 1, 1, 1};
+        if ((rc = encode(&maps.a[0], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem x")))
+            return rc;
+    }
+    {
+        const int planes = split ? 2 : 1;
+        const cuuint64_t dims[5] = {4, (cuuint64_t)K, 8, (cuuint64_t)R, (cuuint64_t)planes};
+        const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)8 * K * 16,
+                                   (cuuint64_t)R * 8 * K * 16};
+        const cuuint32_t box[5] = {4, (cuuint32_t)bn, 8, 1, (cuuint32_t)planes};
+        if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
+            return rc;
+    }
+    pdl::TileParams p{};
+    p.num_kb = R;
+    p.seg_kb = std::max(1, kSegElems / 32);
+    p.n_out = K;
+    p.flags = flags;
+    p.bias = bias;
+    p.out = y;
+    p.nimg = N;
+    p.P = P;
+    p.Q = Q;
+    p.KT = K / 16;
+    p.R = R;
+    p.S = S;
+    p.pad = pad;
+    p.stride = stride;
+    p.CT = 1;
+    p.BW = BW;
+    p.BH = 1;
+    p.BNI = 1;
+    p.box_w = box_w;
+    p.tiles_w = (Q + BW - 1) / BW;
+    p.tiles_h = P;
+    p.m_tiles = p.tiles_w * P * N;
+    p.n_tiles = (K + bn - 1) / bn;
+    dim3 grid(std::min(p.m_tiles * p.n_tiles, sm_count));
+    if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, 1, maps, p, grid, st);
+    return dispatch_tile<pdl::KIND_STEM, false>(bn, 1, maps, p, grid, st);
+}
+
 int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, int N, int C, int K,
                 int H, int W, int R, int S, int stride, int pad, unsigned flags,
                 const pdl_tile_cfg *cfg_in, cudaStream_t st) {
     int rc;
     if ((rc = get_encode())) return rc;
+    if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
+    if (is_stem(C, S, stride))
+        return conv_fwd_stem(x, wp, bias, y, N, C, K, H, W, R, S, stride, pad, flags, cfg_in, st);
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
     conv_default_cfg(C, K, &cfg);
@@ -190,11 +252,9 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         if (cfg_in->bk) cfg.bk = cfg_in->bk;
         cfg.raster = cfg_in->raster;
     }
-    const int CT = C / 16, KT = K / 16, cg = cfg.bk / 16;
+    const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16;
     if (cg < 1 || CT % cg) return fail(PDL_EINVAL, "conv: bk=%d does not divide C=%d", cfg.bk, C);
-    if (K % cfg.bn && cfg.bn > K) cfg.bn = 64;
     const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad);
-    if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
 
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -251,8 +311,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.tiles_h = g.tiles_h;
     p.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
     p.raster = cfg.raster;
-    const int n_tiles = (K + cfg.bn - 1) / cfg.bn;
-    dim3 grid = cfg.raster ? dim3(n_tiles, p.m_tiles) : dim3(p.m_tiles, n_tiles);
+    p.n_tiles = (K + cfg.bn - 1) / cfg.bn;
+    dim3 grid(std::min(p.m_tiles * p.n_tiles, sm_count));
     if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, maps, p, grid, st);
     return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, maps, p, grid, st);
 }
@@ -268,7 +328,8 @@ int pdl_device_check(void) { return device_check(); }
 
 size_t pdl_conv2d_packed_bytes(int C, int K, int R, int S, unsigned flags) {
     const int planes = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 ? 2 : 1;
-    return (size_t)planes * C * K * R * S * sizeof(float);
+    if (is_stem(C, S, 1)) return (size_t)planes * R * 8 * K * 4 * sizeof(float);
+    return (size_t)planes * ceil16(C) * 16 * K * R * S * sizeof(float);
 }
 
 int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R, int S,
@@ -276,13 +337,20 @@ int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
-    if (C % 16 || K % 16 || R <= 0 || S <= 0) return fail(PDL_EINVAL, "prepack: bad shape");
+    if (C <= 0 || K % 16 || K <= 0 || R <= 0 || S <= 0) return fail(PDL_EINVAL, "prepack: bad shape");
     if (!aligned16(w) || !aligned16(packed)) return fail(PDL_EALIGN, "prepack: unaligned pointer");
     const int split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
-    const long long total = (long long)K * C * R * S;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-    pdl::prepack_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-        w, reinterpret_cast<float *>(packed), C / 16, K / 16, R * S, split);
+    if (is_stem(C, S, 1)) {
+        const long long plane = (long long)R * 8 * K * 4;
+        const int blocks = (int)std::min<long long>((plane + 255) / 256, 148LL * 16);
+        pdl::prepack_stem_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            w, reinterpret_cast<float *>(packed), K, R, S, split, C);
+    } else {
+        const long long total = (long long)K * ceil16(C) * 16 * R * S;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+        pdl::prepack_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            w, reinterpret_cast<float *>(packed), ceil16(C), K / 16, R * S, split, C);
+    }
     ++g_launches;
     return check_launch("prepack_weights_kernel");
 }
@@ -318,7 +386,7 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
         const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
         const long long total = (long long)N * (K / 16) * P * Q;
         pdl::simt_conv_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
-            x, w, bias, y, N, C / 16, K / 16, H, W, R, S, stride, pad, P, Q, flags);
+            x, w, bias, y, N, ceil16(C), K / 16, H, W, R, S, stride, pad, P, Q, flags, C);
         ++g_launches;
         return check_launch("simt_conv_kernel");
     }
@@ -389,9 +457,9 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     p.alpha = alpha;
     p.beta = beta;
     p.raster = raster;
-    const int m_tiles = (M + 127) / 128, n_tiles = (N + bn - 1) / bn;
-    p.m_tiles = m_tiles;
-    dim3 grid = raster ? dim3(n_tiles, m_tiles) : dim3(m_tiles, n_tiles);
+    p.m_tiles = (M + 127) / 128;
+    p.n_tiles = (N + bn - 1) / bn;
+    dim3 grid(std::min(p.m_tiles * p.n_tiles, sm_count));
     if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, maps, p, grid, st);
     return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, maps, p, grid, st);
 }

@@ -6,9 +6,12 @@
 //     with the fp32 accumulator in TMEM, and four epilogue warps drain TMEM
 //     through registers, applying the fused bias + ReLU (Alg. 3, PAPER.md:
 //     566-596) before the only store of the output.
-//   * 3xTF32: four "split" warps turn every landed fp32 tile x into
-//     hi = tf32(x) (in place) and lo = x - hi (second buffer); the MMA warp
-//     issues hi*hi + hi*lo + lo*hi.  Conv weights are split once at prepack.
+//   * 3xTF32: four staging warps copy each landed A row into TMEM as
+//     hi = x (the tensor core truncates to tf32) and lo = x - tf32(x); the MMA
+//     warp issues hi*hi + hi*lo + lo*hi with A read from TMEM.  Conv weights
+//     are split once at prepack; the GEMM's B lo is formed in shared memory.
+//   * stem (C <= 4 real channels, e.g. ResNet's 3->64 7x7/2): one TMA halo row
+//     of 4-channel pixels per kernel row; the staging warps gather the taps.
 //   * simt kernels: exact-fp32 CUDA-core GEMM / conv (PDL_MODE_FP32, and the
 //     GEMM path for leading dimensions TMA cannot describe), the unfused
 //     bias+ReLU pass, and the weight prepack.
@@ -26,7 +29,7 @@
 
 namespace pdl {
 
-enum { KIND_GEMM = 0, KIND_CONV = 1 };
+enum { KIND_GEMM = 0, KIND_CONV = 1, KIND_STEM = 2 };
 
 // Geometry / epilogue parameters (by value, param space).
 struct TileParams {
@@ -43,67 +46,72 @@ struct TileParams {
     int nimg, P, Q, KT, R, S, pad, stride, CT;
     int BW, BH, BNI;       // box of output pixels per tile
     int tiles_w, tiles_h;  // tile grid over (Q, P); images fastest-after
+    int box_w;             // stem: input pixels per halo row
     int m_tiles;           // number of M tiles
-    int raster;            // 0: blockIdx.x -> M tile, 1: -> N tile
+    int n_tiles;           // number of N tiles
+    int raster;            // reserved
     int seg_kb;            // k-blocks per TMEM accumulation segment
 };
 
 struct TmaMaps {
-    CUtensorMap a[4];  // conv: one per (row, col) parity for stride 2; GEMM: a[0]
+    CUtensorMap a[4];  // conv: one per (row, col) parity for stride 2; GEMM / stem: a[0]
     CUtensorMap b;
 };
 
+// Shared-memory tiles of one pipeline stage.
+//   GEMM: A [128 rows][32 fp32]   SW128 K-major        B [BN/32][32 k][32 n] SW128_B32 MN-major
+//   CONV: A [CG][128 rows][16]    SW64  K-major        B [CG][BN rows][16]   SW64 K-major
+//   STEM: A [256 px][4 fp32]      halo row, no swizzle B [8 taps][BN][4]     no swizzle K-major
 template <int KIND, int BN, int CG>
 struct Geo {
     static constexpr int BM = 128;
-    // GEMM: A [128 rows][32 fp32] SW128, B [BN/32 chunks][32 k][32 n] SW128 (MN-major)
-    // CONV: A [CG][128 rows][16 fp32] SW64, B [CG][BN rows][16 fp32] SW64 (K-major)
-    static constexpr int A_SUB = KIND == KIND_GEMM ? BM * 128 : BM * 64;
-    static constexpr int B_SUB = KIND == KIND_GEMM ? BN * 128 : BN * 64;
-    static constexpr int NSUB = KIND == KIND_GEMM ? 1 : CG;
+    static constexpr int A_SUB = KIND == KIND_GEMM ? BM * 128 : KIND == KIND_CONV ? BM * 64 : 4096;
+    static constexpr int B_SUB = KIND == KIND_GEMM ? BN * 128 : KIND == KIND_CONV ? BN * 64 : BN * 128;
+    static constexpr int NSUB = KIND == KIND_CONV ? CG : 1;
     static constexpr int A_BYTES = A_SUB * NSUB;
     static constexpr int B_BYTES = B_SUB * NSUB;
-    static constexpr int KK = KIND == KIND_GEMM ? 4 : 2;  // K=8 MMAs per sub-tile
+    static constexpr int KK = KIND == KIND_CONV ? 2 : 4;  // K=8 MMAs per sub-tile
+    static constexpr int KS = KIND == KIND_CONV ? 16 * CG : 32;  // K elements per stage
 };
 
+// TS = A operand staged in TMEM by the split warps (3xTF32, and the stem's tap gather).
 template <int KIND, int BN, int CG, bool SPLIT3>
 struct Smem {
     using G = Geo<KIND, BN, CG>;
-    static constexpr int STAGE = (G::A_BYTES + G::B_BYTES) * (SPLIT3 ? 2 : 1);
-    static constexpr int BUDGET = 200 * 1024;
-    static constexpr int STAGES = (BUDGET / STAGE) > 8 ? 8 : (BUDGET / STAGE);
-    static constexpr int A_HI = 0;
-    static constexpr int A_LO = G::A_BYTES;
-    static constexpr int B_HI = SPLIT3 ? 2 * G::A_BYTES : G::A_BYTES;
+    static constexpr bool TS = SPLIT3 || KIND == KIND_STEM;
+    static constexpr int STAGE = G::A_BYTES + G::B_BYTES * (SPLIT3 ? 2 : 1);
+    static constexpr int BUDGET = 216 * 1024;
+    static constexpr int SLOT_COLS = SPLIT3 ? 2 * G::KS : G::KS;  // TMEM columns per A slot
+    static constexpr int A_SLOT0 = 2 * BN;                        // after the 2 accumulators
+    static constexpr int S_SMEM = BUDGET / STAGE;
+    static constexpr int S_TMEM = TS ? (512 - A_SLOT0) / SLOT_COLS : 8;
+    static constexpr int S0 = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
+    static constexpr int STAGES = S0 > 8 ? 8 : S0;
+    static constexpr int A_OFF = 0;
+    static constexpr int B_HI = G::A_BYTES;
     static constexpr int B_LO = B_HI + G::B_BYTES;
     static constexpr int BAR_OFF = STAGES * STAGE;
     static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + alignment slack
+    static constexpr uint32_t TMEM_COLS = TS ? 512 : 2 * BN;
     static_assert(STAGES >= 2, "tile too large for a 2-stage pipeline");
 };
 
-__device__ __forceinline__ float4 split_hi(float4 v) {
-    float4 h;
-    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-    return h;
+__device__ __forceinline__ float tf32_lo(float x) {
+    // the tensor core truncates fp32 operands to tf32 (probed on B200), so the
+    // hi part is x itself and lo = x - trunc_tf32(x), exact in fp32
+    return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// In-place hi + separate lo over `bytes` of shared memory (layout-agnostic:
-// the transform is element-wise, so the swizzled tile stays swizzled).
-__device__ __forceinline__ void split_tile(uint8_t *hi, uint8_t *lo, int bytes, int tid,
-                                           int nthreads) {
-    float4 *h4 = reinterpret_cast<float4 *>(hi);
+// lo = x - tf32(x) for `bytes` of shared memory (element-wise, layout-agnostic).
+__device__ __forceinline__ void split_lo_smem(const uint8_t *src, uint8_t *lo, int bytes, int tid,
+                                              int nthreads) {
+    const float4 *s4 = reinterpret_cast<const float4 *>(src);
     float4 *l4 = reinterpret_cast<float4 *>(lo);
     const int n = bytes >> 4;
 #pragma unroll 4
     for (int i = tid; i < n; i += nthreads) {
-        float4 v = h4[i];
-        float4 h = split_hi(v);
-        float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        h4[i] = h;
-        l4[i] = l;
+        const float4 v = s4[i];
+        l4[i] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
     }
 }
 
@@ -140,24 +148,68 @@ __device__ __forceinline__ void store16(const TileParams &p, float *dst, int col
     }
 }
 
-// Implicit-GEMM tile engine.  One CTA = one 128 x BN output tile.
-//   warp 0      TMA producer (one lane)
-//   warp 1      tcgen05.mma issuer (one lane)
-//   warp 2      TMEM allocator
-//   warps 4-7   3xTF32 split of each landed stage, then TMEM drain + epilogue
-// The reduction is cut into segments of p.seg_kb k-blocks; each segment is
-// accumulated in one of two TMEM buffers (ping-pong) and drained into fp32
-// registers with round-to-nearest adds.  The tensor core's accumulator
+// Persistent implicit-GEMM tile engine.  gridDim.x CTAs (<= #SMs), one per SM;
+// CTA b processes tiles b, b + gridDim.x, ... (N-tiles fastest so concurrent
+// CTAs share activation rows through L2).
+//   warp 0       TMA producer (one lane), runs ahead across tile boundaries
+//   warp 1       tcgen05.mma issuer (one lane)
+//   warp 2       TMEM allocator
+//   warps 4-7    A staging (TS modes): thread = tile row = TMEM lane; reads its
+//                row of the landed tile (conv: gathers the stem's taps), writes
+//                hi (= x, the tensor core truncates) and lo = x - tf32(x) into a
+//                TMEM A slot with tcgen05.st; GEMM also forms B's lo in smem
+//   warps 8-15   TMEM drain + epilogue; warp 8+e owns TMEM lanes 32*(e%4).. and
+//                output columns [(e/4)*BN/2, (e/4+1)*BN/2)
+// 3xTF32 issues hi*hi + hi*lo + lo*hi per K=8 step.  The reduction of every tile
+// is cut into segments of p.seg_kb k-blocks; each segment accumulates in one of
+// two TMEM buffers (ping-pong, continuing across tiles) and is drained into
+// fp32 registers with round-to-nearest adds.  The tensor core's accumulator
 // truncates, so an unsegmented K=4096 sum drifts to ~3e-5 relative error;
-// 256-element segments keep it near 3e-6 at any K.
+// 256-element segments keep it near 3e-6 at any K.  The ping-pong also lets
+// tile i's epilogue overlap tile i+1's first segment.
+constexpr int kThreads = 512;
+constexpr int kSplitWarp0 = 4;
+constexpr int kEpiWarp0 = 8;
+constexpr int kEpiThreads = 256;
+
+struct TileCoord {
+    int n0;          // first output column
+    int m0;          // GEMM: first row
+    int q0, p0, i0;  // conv: first output col / row / image of the pixel box
+};
+
+template <int KIND, int BN>
+__device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
+    TileCoord c;
+    const int mt = tile / p.n_tiles;
+    c.n0 = (tile - mt * p.n_tiles) * BN;
+    c.m0 = 0;
+    c.q0 = 0;
+    c.p0 = 0;
+    c.i0 = 0;
+    if (KIND == KIND_GEMM) {
+        c.m0 = mt * 128;
+    } else {
+        int t = mt;
+        const int tw = t % p.tiles_w;
+        t /= p.tiles_w;
+        const int th = t % p.tiles_h;
+        t /= p.tiles_h;
+        c.q0 = tw * p.BW;
+        c.p0 = th * p.BH;
+        c.i0 = t * p.BNI;
+    }
+    return c;
+}
+
 template <int KIND, int BN, int CG, bool SPLIT3>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
     using G = Geo<KIND, BN, CG>;
     using L = Smem<KIND, BN, CG, SPLIT3>;
+    constexpr bool TS = L::TS;
     constexpr int STAGES = L::STAGES;
-    constexpr bool SEGMENTED = BN <= 128;  // register budget for the running sums
-    constexpr uint32_t TMEM_COLS = SEGMENTED ? 2 * BN : BN;
+    constexpr int HALF = BN / 2;  // columns per epilogue warp
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem =
         reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -170,15 +222,17 @@ __global__ void __launch_bounds__(256, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m_tile = p.raster ? blockIdx.y : blockIdx.x;
-    const int n_tile = p.raster ? blockIdx.x : blockIdx.y;
-    const int n0 = n_tile * BN;
-    const int seg_kb = SEGMENTED ? p.seg_kb : p.num_kb;
-    const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
+    const int num_tiles = p.m_tiles * p.n_tiles;
+    const int seg_kb = p.seg_kb;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&maps.b);
         tma_prefetch(&maps.a[0]);
+        if (KIND == KIND_CONV && p.stride == 2) {
+            tma_prefetch(&maps.a[1]);
+            tma_prefetch(&maps.a[2]);
+            tma_prefetch(&maps.a[3]);
+        }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&ready[s], 128);
@@ -186,221 +240,263 @@ __global__ void __launch_bounds__(256, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full[b], 1);
-            mbar_init(&tmem_empty[b], 128);
+            mbar_init(&tmem_empty[b], kEpiThreads);
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 2) tmem_alloc<L::TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    // Conv tile origin (shared by producer and epilogue).
-    int q0 = 0, p0 = 0, i0 = 0, m0 = 0;
-    if (KIND == KIND_CONV) {
-        int t = m_tile;
-        const int tw = t % p.tiles_w;
-        t /= p.tiles_w;
-        const int th = t % p.tiles_h;
-        t /= p.tiles_h;
-        q0 = tw * p.BW;
-        p0 = th * p.BH;
-        i0 = t * p.BNI;
-    } else {
-        m0 = m_tile * G::BM;
-    }
-
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
-            const uint32_t tx =
-                KIND == KIND_GEMM
-                    ? (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4)
-                    : (uint32_t)(CG * 64 * p.BW * p.BH * p.BNI + CG * BN * 64 * (SPLIT3 ? 2 : 1));
+            uint32_t tx;
+            if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
+            else if (KIND == KIND_CONV)
+                tx = (uint32_t)(CG * 64 * p.BW * p.BH * p.BNI + CG * BN * 64 * (SPLIT3 ? 2 : 1));
+            else tx = (uint32_t)(16 * p.box_w + BN * 128 * (SPLIT3 ? 2 : 1));
             int s = 0;
             uint32_t ph = 0;
-            for (int kb = 0; kb < p.num_kb; ++kb) {
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t *st = smem + s * L::STAGE;
-                mbar_arrive_expect_tx(&full[s], tx);
-                if (KIND == KIND_GEMM) {
-                    tma_load_2d(st + L::A_HI, &maps.a[0], &full[s], kb * 32, m0);
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const TileCoord tc = tile_coord<KIND, BN>(p, tile);
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t *st = smem + s * L::STAGE;
+                    mbar_arrive_expect_tx(&full[s], tx);
+                    if (KIND == KIND_GEMM) {
+                        tma_load_2d(st + L::A_OFF, &maps.a[0], &full[s], kb * 32, tc.m0);
 #pragma unroll
-                    for (int c = 0; c < BN / 32; ++c)
-                        tma_load_2d(st + L::B_HI + c * 4096, &maps.b, &full[s], n0 + c * 32,
-                                    kb * 32);
-                } else {
-                    const int rs_n = p.R * p.S;
-                    const int ctg = kb / rs_n;
-                    const int rs = kb - ctg * rs_n;
-                    const int r = rs / p.S;
-                    const int sx = rs - r * p.S;
-                    int dh = r - p.pad, dw = sx - p.pad, mi = 0;
-                    if (p.stride == 2) {
-                        const int ph2 = dh & 1, pw2 = dw & 1;
-                        mi = ph2 * 2 + pw2;
-                        dh = (dh - ph2) >> 1;
-                        dw = (dw - pw2) >> 1;
+                        for (int c = 0; c < BN / 32; ++c)
+                            tma_load_2d(st + L::B_HI + c * 4096, &maps.b, &full[s], tc.n0 + c * 32,
+                                        kb * 32);
+                    } else if (KIND == KIND_CONV) {
+                        const int rs_n = p.R * p.S;
+                        const int ctg = kb / rs_n;
+                        const int rs = kb - ctg * rs_n;
+                        const int r = rs / p.S;
+                        const int sx = rs - r * p.S;
+                        int dh = r - p.pad, dw = sx - p.pad, mi = 0;
+                        if (p.stride == 2) {
+                            const int ph2 = dh & 1, pw2 = dw & 1;
+                            mi = ph2 * 2 + pw2;
+                            dh = (dh - ph2) >> 1;
+                            dw = (dw - pw2) >> 1;
+                        }
+#pragma unroll
+                        for (int c = 0; c < CG; ++c)
+                            tma_load_5d(st + L::A_OFF + c * G::A_SUB, &maps.a[mi], &full[s], 0,
+                                        tc.q0 + dw, tc.p0 + dh, ctg * CG + c, tc.i0);
+                        tma_load_5d(st + L::B_HI, &maps.b, &full[s], 0, tc.n0, rs, ctg * CG, 0);
+                    } else {
+                        // stem: k-block = kernel row r; one halo row of 4-channel pixels
+                        tma_load_5d(st + L::A_OFF, &maps.a[0], &full[s], 0,
+                                    tc.q0 * p.stride - p.pad, tc.p0 * p.stride + kb - p.pad, 0, tc.i0);
+                        tma_load_5d(st + L::B_HI, &maps.b, &full[s], 0, tc.n0, 0, kb, 0);
                     }
-#pragma unroll
-                    for (int c = 0; c < CG; ++c)
-                        tma_load_5d(st + L::A_HI + c * G::A_SUB, &maps.a[mi], &full[s], 0,
-                                    q0 + dw, p0 + dh, ctg * CG + c, i0);
-                    tma_load_5d(st + L::B_HI, &maps.b, &full[s], 0, n0, rs, ctg * CG, 0);
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
-                if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (one thread) =====================
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(128, BN, KIND == KIND_GEMM ? 1 : 0);
-            const uint32_t layout = KIND == KIND_GEMM ? LAYOUT_SW128 : LAYOUT_SW64;
-            const uint32_t a_sbo = KIND == KIND_GEMM ? 1024 : 512;
             const uint32_t smem0 = smem_u32(smem);
             int s = 0;
             uint32_t ph = 0;
-            int g = 0, in_seg = 0;
-            uint32_t d_tmem = tmem_base;
-            for (int kb = 0; kb < p.num_kb; ++kb) {
-                if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
-                    mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
+            int g = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int in_seg = 0;
+                uint32_t d_tmem = tmem_base;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
+                        mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
+                        tc_fence_after();
+                        d_tmem = tmem_base + (uint32_t)((g & 1) * BN);
+                    }
+                    mbar_wait(TS ? &ready[s] : &full[s], ph);
                     tc_fence_after();
-                    d_tmem = tmem_base + (SEGMENTED ? (uint32_t)((g & 1) * BN) : 0u);
-                }
-                mbar_wait(SPLIT3 ? &ready[s] : &full[s], ph);
-                tc_fence_after();
-                const uint32_t st = smem0 + s * L::STAGE;
+                    const uint32_t st = smem0 + s * L::STAGE;
+                    const uint32_t a_t = tmem_base + L::A_SLOT0 + s * L::SLOT_COLS;
 #pragma unroll
-                for (int c = 0; c < G::NSUB; ++c) {
+                    for (int c = 0; c < G::NSUB; ++c) {
 #pragma unroll
-                    for (int kk = 0; kk < G::KK; ++kk) {
-                        const uint32_t a_off = c * G::A_SUB + kk * 32;
-                        const uint64_t ahi = smem_desc(st + L::A_HI + a_off, 16, a_sbo, layout);
-                        const uint64_t alo = smem_desc(st + L::A_LO + a_off, 16, a_sbo, layout);
-                        uint64_t bhi, blo;
-                        if (KIND == KIND_GEMM) {
-                            // MN-major tf32 operand: 128B rows of 32 n-values, 32B-atom
-                            // swizzle (layout SWIZZLE_128B_BASE32B); 4-row k-groups at
-                            // SBO = 512B, 32-col chunks at LBO = 32 rows * 128B.
-                            bhi = smem_desc(st + L::B_HI + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
-                            blo = smem_desc(st + L::B_LO + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
-                        } else {
-                            const uint32_t b_off = c * G::B_SUB + kk * 32;
-                            bhi = smem_desc(st + L::B_HI + b_off, 16, 512, LAYOUT_SW64);
-                            blo = smem_desc(st + L::B_LO + b_off, 16, 512, LAYOUT_SW64);
-                        }
-                        const uint32_t acc = (in_seg | c | kk) != 0;
-                        mma_tf32(d_tmem, ahi, bhi, idesc, acc);
-                        if (SPLIT3) {
-                            mma_tf32(d_tmem, ahi, blo, idesc, 1);
-                            mma_tf32(d_tmem, alo, bhi, idesc, 1);
+                        for (int kk = 0; kk < G::KK; ++kk) {
+                            uint64_t bhi, blo;
+                            if (KIND == KIND_GEMM) {
+                                // MN-major tf32 operand: 128B rows of 32 n-values, 32B-atom
+                                // swizzle (SWIZZLE_128B_BASE32B); 4-row k-groups at SBO = 512B,
+                                // 32-col chunks at LBO = 32 rows * 128B.
+                                bhi = smem_desc(st + L::B_HI + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
+                                blo = smem_desc(st + L::B_LO + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
+                            } else if (KIND == KIND_CONV) {
+                                const uint32_t b_off = c * G::B_SUB + kk * 32;
+                                bhi = smem_desc(st + L::B_HI + b_off, 16, 512, LAYOUT_SW64);
+                                blo = smem_desc(st + L::B_LO + b_off, 16, 512, LAYOUT_SW64);
+                            } else {
+                                // no-swizzle K-major: 8-row x 16B core matrices; taps
+                                // (2kk, 2kk+1) are two core-matrix columns BN*16 B apart
+                                const uint32_t b_off = kk * 2 * BN * 16;
+                                bhi = smem_desc(st + L::B_HI + b_off, BN * 16, 128, 0);
+                                blo = smem_desc(st + L::B_LO + b_off, BN * 16, 128, 0);
+                            }
+                            const uint32_t acc = (in_seg | c | kk) != 0;
+                            if (TS) {
+                                const uint32_t ahi = a_t + c * 16 + kk * 8;
+                                mma_tf32_ts(d_tmem, ahi, bhi, idesc, acc);
+                                if (SPLIT3) {
+                                    mma_tf32_ts(d_tmem, ahi, blo, idesc, 1);
+                                    mma_tf32_ts(d_tmem, ahi + G::KS, bhi, idesc, 1);
+                                }
+                            } else {
+                                const uint32_t layout = KIND == KIND_GEMM ? LAYOUT_SW128 : LAYOUT_SW64;
+                                const uint32_t a_sbo = KIND == KIND_GEMM ? 1024 : 512;
+                                const uint32_t a_off = c * G::A_SUB + kk * 32;
+                                const uint64_t ahi = smem_desc(st + L::A_OFF + a_off, 16, a_sbo, layout);
+                                mma_tf32(d_tmem, ahi, bhi, idesc, acc);
+                            }
                         }
                     }
-                }
-                mma_commit(&empty[s]);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
-                if (++in_seg == seg_kb || kb + 1 == p.num_kb) {
-                    mma_commit(&tmem_full[g & 1]);
-                    in_seg = 0;
-                    ++g;
+                    mma_commit(&empty[s]);
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                    if (++in_seg == seg_kb || kb + 1 == p.num_kb) {
+                        mma_commit(&tmem_full[g & 1]);
+                        in_seg = 0;
+                        ++g;
+                    }
                 }
             }
         }
-    } else if (warp >= 4) {
-        const int tid = threadIdx.x - 128;
-        const int quarter = warp - 4;
+    } else if (warp >= kSplitWarp0 && warp < kEpiWarp0) {
+        // ===================== A staging into TMEM (hi / lo) =====================
+        if (TS) {
+            const int tid = threadIdx.x - kSplitWarp0 * 32;
+            const int quarter = warp - kSplitWarp0;
+            const int row = quarter * 32 + lane;
+            const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint8_t *sa = smem + s * L::STAGE + L::A_OFF;
+                    const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + s * L::SLOT_COLS;
+                    if (KIND == KIND_GEMM) {
+                        float x[32], lo[32];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 v = *reinterpret_cast<const float4 *>(
+                                sa + row * 128 + ((j ^ (row & 7)) << 4));
+                            x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
+                        tmem_st32(t_hi, x);
+                        tmem_st32(t_hi + G::KS, lo);
+                        split_lo_smem(smem + s * L::STAGE + L::B_HI, smem + s * L::STAGE + L::B_LO,
+                                      G::B_BYTES, tid, 128);
+                        fence_proxy_async_smem();
+                    } else if (KIND == KIND_CONV) {
+#pragma unroll
+                        for (int c = 0; c < CG; ++c) {
+                            float x[16], lo[16];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const float4 v = *reinterpret_cast<const float4 *>(
+                                    sa + c * G::A_SUB + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
+                                x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) lo[i] = tf32_lo(x[i]);
+                            tmem_st16(t_hi + c * 16, x);
+                            if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
+                        }
+                    } else {
+                        // stem: gather taps s = 0..S-1 (4 channels each) of this output pixel
+                        float x[32], lo[32];
+                        const bool live = row < p.BW;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (live && t < p.S)
+                                v = *reinterpret_cast<const float4 *>(sa + (row * p.stride + t) * 16);
+                            x[4 * t] = v.x; x[4 * t + 1] = v.y; x[4 * t + 2] = v.z; x[4 * t + 3] = v.w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
+                        tmem_st32(t_hi, x);
+                        if (SPLIT3) tmem_st32(t_hi + G::KS, lo);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&ready[s]);
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ===================== TMEM drain + epilogue =====================
+        const int e = warp - kEpiWarp0;
+        const int quarter = e & 3;
+        const int half = e >> 2;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        float sum[SEGMENTED ? BN : 1];
-        if (SEGMENTED) {
+        const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
+        int g = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const TileCoord tc = tile_coord<KIND, BN>(p, tile);
+            float sum[HALF];
 #pragma unroll
-            for (int i = 0; i < (SEGMENTED ? BN : 1); ++i) sum[i] = 0.f;
-        }
-        int drained = 0;
-        auto drain = [&](int g) {
-            mbar_wait(&tmem_full[g & 1], (g >> 1) & 1);
-            tc_fence_after();
-            if (SEGMENTED) {
-                const uint32_t base = tmem_base + lane_off + (uint32_t)((g & 1) * BN);
+            for (int i = 0; i < HALF; ++i) sum[i] = 0.f;
+            for (int sg = 0; sg < nseg; ++sg, ++g) {
+                mbar_wait(&tmem_full[g & 1], (g >> 1) & 1);
+                tc_fence_after();
+                const uint32_t base = tmem_base + lane_off + (uint32_t)((g & 1) * BN + half * HALF);
 #pragma unroll
-                for (int j = 0; j < BN / 16; ++j) {
+                for (int j = 0; j < HALF / 16; ++j) {
                     float v[16];
                     tmem_ld16(base + j * 16, v);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) sum[(SEGMENTED ? j * 16 + i : 0)] += v[i];
+                    for (int i = 0; i < 16; ++i) sum[j * 16 + i] += v[i];
                 }
                 tc_fence_before();
                 mbar_arrive(&tmem_empty[g & 1]);
             }
-        };
-        const int a_valid = KIND == KIND_GEMM ? G::A_SUB : 64 * p.BW * p.BH * p.BNI;
-        {
-            int s = 0;
-            uint32_t ph = 0;
-            for (int kb = 0; kb < p.num_kb; ++kb) {
-                if (SPLIT3) {
-                    // ===================== 3xTF32 split =====================
-                    mbar_wait(&full[s], ph);
-                    uint8_t *st = smem + s * L::STAGE;
-#pragma unroll
-                    for (int c = 0; c < G::NSUB; ++c)
-                        split_tile(st + L::A_HI + c * G::A_SUB, st + L::A_LO + c * G::A_SUB,
-                                   a_valid, tid, 128);
-                    if (KIND == KIND_GEMM)
-                        split_tile(st + L::B_HI, st + L::B_LO, G::B_BYTES, tid, 128);
-                    fence_proxy_async_smem();
-                    mbar_arrive(&ready[s]);
-                    if (++s == STAGES) { s = 0; ph ^= 1; }
-                }
-                // drain segments that finished at least one k-block ago
-                if (SEGMENTED && drained < nseg - 1 && kb >= (drained + 1) * seg_kb) drain(drained++);
+            // ---- store (bias + ReLU fused) ----
+            bool valid;
+            float *obase;
+            size_t cstride = 0;
+            if (KIND == KIND_GEMM) {
+                const int gm = tc.m0 + row;
+                valid = gm < p.M;
+                obase = p.out + (size_t)(valid ? gm : 0) * p.ldc;
+            } else {
+                const int per_img = p.BW * p.BH;
+                const int il = row / per_img;
+                const int rem = row - il * per_img;
+                const int hl = rem / p.BW;
+                const int wl = rem - hl * p.BW;
+                const int img = tc.i0 + il, pp = tc.p0 + hl, qq = tc.q0 + wl;
+                valid = il < p.BNI && img < p.nimg && pp < p.P && qq < p.Q;
+                const size_t plane = (size_t)p.P * p.Q * 16;
+                obase = p.out + ((size_t)(valid ? img : 0) * p.KT) * plane +
+                        ((size_t)(valid ? pp : 0) * p.Q + (valid ? qq : 0)) * 16;
+                cstride = plane;  // next 16-channel block kt
             }
-        }
-        // ===================== epilogue =====================
-        bool valid;
-        float *obase = nullptr;
-        size_t cstride = 0;
-        if (KIND == KIND_GEMM) {
-            const int gm = m0 + row;
-            valid = gm < p.M;
-            obase = p.out + (size_t)(valid ? gm : 0) * p.ldc;
-        } else {
-            const int per_img = p.BW * p.BH;
-            const int il = row / per_img;
-            const int rem = row - il * per_img;
-            const int hl = rem / p.BW;
-            const int wl = rem - hl * p.BW;
-            const int img = i0 + il, pp = p0 + hl, qq = q0 + wl;
-            valid = il < p.BNI && img < p.nimg && pp < p.P && qq < p.Q;
-            const size_t plane = (size_t)p.P * p.Q * 16;
-            obase = p.out + ((size_t)(valid ? img : 0) * p.KT) * plane +
-                    ((size_t)(valid ? pp : 0) * p.Q + (valid ? qq : 0)) * 16;
-            cstride = plane;  // next 16-channel block kt
-        }
-        if (SEGMENTED) {
-            while (drained < nseg) drain(drained++);
             if (valid) {
 #pragma unroll
-                for (int j = 0; j < BN / 16; ++j) {
-                    const int col0 = n0 + j * 16;
+                for (int j = 0; j < HALF / 16; ++j) {
+                    const int col0 = tc.n0 + half * HALF + j * 16;
                     if (col0 < p.n_out) {
-                        float *dst = KIND == KIND_GEMM ? obase + col0 : obase + (size_t)(col0 >> 4) * cstride;
-                        store16<KIND>(p, dst, col0, &sum[SEGMENTED ? j * 16 : 0]);
+                        float *dst = KIND == KIND_GEMM ? obase + col0
+                                                       : obase + (size_t)(col0 >> 4) * cstride;
+                        store16<KIND>(p, dst, col0, &sum[j * 16]);
                     }
                 }
-            }
-        } else {
-            drain(0);
-#pragma unroll 1
-            for (int j = 0; j < BN / 16; ++j) {
-                float v[16];
-                tmem_ld16(tmem_base + lane_off + j * 16, v);
-                const int col0 = n0 + j * 16;
-                if (!valid || col0 >= p.n_out) continue;
-                float *dst = KIND == KIND_GEMM ? obase + col0 : obase + (size_t)(col0 >> 4) * cstride;
-                store16<KIND>(p, dst, col0, v);
             }
         }
     }
@@ -409,7 +505,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
+        tmem_dealloc<L::TMEM_COLS>(tmem_base);
     }
 }
 
@@ -476,7 +572,7 @@ __global__ void __launch_bounds__(128) simt_conv_kernel(const float *__restrict_
                                                         float *__restrict__ y, int N, int CT,
                                                         int KT, int H, int W, int R, int S,
                                                         int stride, int pad, int P, int Q,
-                                                        unsigned flags) {
+                                                        unsigned flags, int C_real) {
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long total = (long long)N * KT * P * Q;
     if (idx >= total) return;
@@ -495,6 +591,7 @@ __global__ void __launch_bounds__(128) simt_conv_kernel(const float *__restrict_
                 const float *xi = x + ((((size_t)n * CT + ct) * H + ih) * W + iw) * 16;
                 const float *wb = w + ((((size_t)kt * CT + ct) * R + r) * S + s) * 256;
                 for (int c = 0; c < 16; ++c) {
+                    if (ct * 16 + c >= C_real) break;
                     const float a = xi[c];
 #pragma unroll
                     for (int k = 0; k < 16; ++k) acc[k] = fmaf(__ldg(wb + c * 16 + k), a, acc[k]);
@@ -533,10 +630,11 @@ __global__ void bias_relu_kernel(float4 *__restrict__ y, const float4 *__restric
 }
 
 // Weight prepack KCRS16c16k -> packed[plane][ct][r*S+s][k][c] (K-major rows of
-// 16 input channels per output channel k); plane 0 = hi (or raw for TF32),
-// plane 1 = lo = w - tf32(w) for 3xTF32.
+// 16 input channels per output channel k); plane 0 = w (the tensor core
+// truncates to tf32), plane 1 = lo = w - tf32(w) for 3xTF32.  Input channels
+// >= C_real are zeroed (nChw16c pads C to a multiple of 16).
 __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__restrict__ out,
-                                       int CT, int KT, int RS, int split) {
+                                       int CT, int KT, int RS, int split, int C_real) {
     const long long total = (long long)KT * CT * RS * 256;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -548,15 +646,31 @@ __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__res
         t /= RS;
         const int ct = t % CT;
         const int kt = (int)(t / CT);
-        const float v = w[i];
+        const float v = (ct * 16 + c < C_real) ? w[i] : 0.f;
         const size_t dst = ((((size_t)ct * RS + rs) * (KT * 16)) + (size_t)kt * 16 + k) * 16 + c;
-        if (split) {
-            const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-            out[dst] = h;
-            out[dst + total] = v - h;
-        } else {
-            out[dst] = v;
-        }
+        out[dst] = v;
+        if (split) out[dst + total] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    }
+}
+
+// Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[plane][r][tap 0..7][k][4 c]
+// (no-swizzle K-major core matrices); taps >= S and channels >= C_real are zero.
+__global__ void prepack_stem_weights_kernel(const float *__restrict__ w, float *__restrict__ out,
+                                            int K, int R, int S, int split, int C_real) {
+    const long long plane = (long long)R * 8 * K * 4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = i & 3;
+        long long t = i >> 2;
+        const int k = t % K;
+        t /= K;
+        const int tap = t % 8;
+        const int r = (int)(t / 8);
+        float v = 0.f;
+        if (tap < S && c < C_real)
+            v = w[((((size_t)(k >> 4) * R + r) * S + tap) * 16 + c) * 16 + (k & 15)];
+        out[i] = v;
+        if (split) out[i + plane] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     }
 }
 

@@ -68,11 +68,17 @@ class PackedWeights:
     mode: str
 
 
-def prepack_weights(w: torch.Tensor, mode: str = "3xtf32", stream=None) -> PackedWeights:
+def prepack_weights(w: torch.Tensor, mode: str = "3xtf32", channels: int | None = None,
+                    stream=None) -> PackedWeights:
+    """One-time reorder of KCRS16c16k weights into the tensor-core operand image.
+    `channels` = true input channels C when the last 16-block is padded (the
+    ResNet stem has C=3 stored in one 16-channel block)."""
     _need_cuda_f32("w", w)
     kt, ct, r, s, c16, k16 = w.shape
     assert c16 == 16 and k16 == 16, "weights must be KCRS16c16k"
-    C, K = ct * 16, kt * 16
+    C, K = (channels if channels is not None else ct * 16), kt * 16
+    if not (ct * 16 - 16 < C <= ct * 16):
+        raise ValueError(f"channels={C} inconsistent with {ct} channel blocks")
     flags = _mode(mode)
     nbytes = lib().pdl_conv2d_packed_bytes(C, K, r, s, flags)
     out = torch.empty(nbytes // 4, dtype=torch.float32, device=w.device)
@@ -83,9 +89,12 @@ def prepack_weights(w: torch.Tensor, mode: str = "3xtf32", stream=None) -> Packe
 
 def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride: int = 1,
                    pad: int = 0, relu: bool = False, mode: str = "3xtf32", cfg=None,
-                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                   out: torch.Tensor | None = None, channels: int | None = None,
+                   stream=None) -> torch.Tensor:
     """Blocked conv fwd (+bias, +ReLU fused in the epilogue).  `w` is either raw
-    KCRS16c16k weights or a PackedWeights from prepack_weights()."""
+    KCRS16c16k weights or a PackedWeights from prepack_weights().  `channels` =
+    true input channels when x's last 16-channel block is zero-padded (C <= 4
+    selects the narrow stem kernel)."""
     _need_cuda_f32("x", x)
     _need_cuda_f32("bias", bias)
     n, ct, h, wd, v = x.shape
@@ -99,9 +108,11 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
     else:
         _need_cuda_f32("w", w)
         kt, ct2, R, S, _, _ = w.shape
-        C, K = ct2 * 16, kt * 16
-    if C != ct * 16:
-        raise ValueError(f"channel mismatch: x has {ct * 16}, w has {C}")
+        C, K = (channels if channels is not None else ct2 * 16), kt * 16
+    if channels is not None and channels != C:
+        raise ValueError(f"channels={channels} but weights were packed for C={C}")
+    if not (ct * 16 - 16 < C <= ct * 16):
+        raise ValueError(f"channel mismatch: x has {ct} blocks of 16, w has C={C}")
     P, Q = conv_out_hw(h, wd, R, S, stride, pad)
     y = out if out is not None else torch.empty((n, K // 16, P, Q, 16), dtype=torch.float32,
                                                 device=x.device)

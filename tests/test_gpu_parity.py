@@ -112,14 +112,14 @@ def _conv_ref(layer, n, relu, images=None):
 def test_resnet_layer_fused(P, layer, mode):
     x, w, b, ref = _conv_ref(layer, 2, True)
     y = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=layer.stride, pad=layer.pad,
-                         relu=True, mode=mode)
+                         relu=True, mode=mode, channels=layer.C)
     assert rel(y.cpu().numpy(), ref) <= TOL[mode]
 
 
 @pytest.mark.parametrize("layer", W.LAYERS, ids=lambda l: l.name())
 def test_resnet_layer_unfused_and_prepacked(P, layer):
     x, w, b, ref = _conv_ref(layer, 2, True)
-    pw = P.prepack_weights(cuda(w), mode="3xtf32")
+    pw = P.prepack_weights(cuda(w), mode="3xtf32", channels=layer.C)
     y = P.conv2d_nchw16c(cuda(x), pw, None, stride=layer.stride, pad=layer.pad)
     P.bias_relu_(y, cuda(b))
     assert rel(y.cpu().numpy(), ref) <= 1e-5
@@ -133,7 +133,7 @@ def test_resnet_layer_full_batch_sampled_images(P, layer):
     n = 28
     x, w, b = W.conv_inputs(layer, n, seed=500 + layer.idx)
     y = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=layer.stride, pad=layer.pad,
-                         relu=True).cpu().numpy()
+                         relu=True, channels=layer.C).cpu().numpy()
     for img in (0, n - 1):
         ref = oracle.conv2d_f64(x, w, b, stride=layer.stride, pad=layer.pad, relu=True,
                                 images=(img, 1))
@@ -188,6 +188,24 @@ def test_ragged_spatial(P, h, r, stride):
     ref = oracle.conv2d_f64(x, w, b, stride=stride, pad=layer.pad, relu=True)
     y = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=stride, pad=layer.pad, relu=True)
     assert rel(y.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("c,r,stride,h", [(3, 7, 2, 30), (4, 3, 1, 9), (1, 5, 2, 11), (3, 7, 2, 224)])
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32", "fp32"])
+def test_narrow_channel_stem(P, c, r, stride, h, mode):
+    """C <= 4 real channels in one padded 16-block: the stem kernel must ignore
+    the padding channels even if they hold garbage."""
+    layer = W.ConvLayer(98, c, 64 if h != 224 else 128, h, r, stride)
+    n = 2 if h < 224 else 1
+    x, w, b = W.conv_inputs(layer, n, seed=c * 100 + r)
+    ref = oracle.conv2d_f64(x, w, b, stride=stride, pad=layer.pad, relu=True)
+    xg = x.copy()
+    xg[..., c:] = 7.0  # garbage in the padding channels must not leak in
+    wg = w.copy()
+    wg[:, :, :, :, c:, :] = -3.0
+    y = P.conv2d_nchw16c(cuda(xg), cuda(wg), cuda(b), stride=stride, pad=layer.pad, relu=True,
+                         mode=mode, channels=c)
+    assert rel(y.cpu().numpy(), ref) <= TOL[mode]
 
 
 def test_bad_shapes_raise(P):
