@@ -44,6 +44,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
+    ap.add_argument("--cluster", type=int, default=0, help="override CTAs per weight-multicast cluster")
     return ap.parse_args()
 
 
@@ -233,6 +234,7 @@ def run_suite(args, rank, world, local):
 
     stream = torch.cuda.current_stream()
     launches_per_step = 0
+    cfg = {"cluster_m": args.cluster} if args.cluster else None
 
     def step(ev=None):
         nonlocal launches_per_step
@@ -241,7 +243,7 @@ def run_suite(args, rank, world, local):
             if ev is not None:
                 ev[i][0].record(stream)
             P.conv2d_nchw16c(x, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
-                             mode=args.mode, out=y)
+                             mode=args.mode, out=y, cfg=cfg)
             cnt += _lib.last_launch_count()
             if ev is not None:
                 ev[i][1].record(stream)
@@ -433,6 +435,7 @@ def run_gemm(args, rank, world, local):
     peaks = load_peaks()
     mode_peak = peaks["tf32_tflops"] * 1e12 / (3.0 if args.mode == "3xtf32" else 1.0)
     stream = torch.cuda.current_stream()
+    gcfg = {"cluster_m": args.cluster} if args.cluster else None
     rows, tot_f, tot_ms = [], 0.0, 0.0
     for (m, n, k) in W.GEMM_SWEEP:
         g = torch.Generator(device="cuda")
@@ -444,7 +447,7 @@ def run_gemm(args, rank, world, local):
         flush = torch.empty(64 * 1024 * 1024, device="cuda")  # 256 MB > L2
         for i in range(args.warmup):
             a, b, c = sets[i % 4]
-            P.gemm(a, b, c, mode=args.mode)
+            P.gemm(a, b, c, mode=args.mode, cfg=gcfg)
         ms = 0.0
         for i in range(args.steps):
             flush.zero_()
@@ -452,7 +455,7 @@ def run_gemm(args, rank, world, local):
             a, b, c = sets[i % 4]
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            P.gemm(a, b, c, mode=args.mode)
+            P.gemm(a, b, c, mode=args.mode, cfg=gcfg)
             e1.record(stream)
             torch.cuda.synchronize()
             ms += e0.elapsed_time(e1)

@@ -42,6 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            os.path.join(SRC, "pdl_capi.cu")]
     if verbose:
         cmd.insert(4, "-Xptxas=-v")
+    if os.environ.get("PDL_WATCHDOG"):
+        cmd.insert(4, "-DPDL_WATCHDOG=1")
     env = dict(os.environ)
     if os.path.exists("/usr/bin/g++"):
         cmd[1:1] = ["-ccbin", "/usr/bin/g++"]

@@ -58,11 +58,12 @@ int get_encode() {
 
 int encode(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
            const cuuint64_t *strides_bytes, const cuuint32_t *box, CUtensorMapSwizzle sw,
-           const char *what) {
+           const char *what,
+           CUtensorMapL2promotion l2 = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void *>(base),
-                          dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, l2,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PDL_EINVAL, "tensor map encode failed (%s, rc=%d)", what, (int)r);
     return PDL_OK;
 }
@@ -87,42 +88,88 @@ int device_check() {
 
 // Reduction elements accumulated in TMEM before an fp32 round-to-nearest drain.
 constexpr int kSegElems = 256;
+// CTAs per cluster sharing (multicasting) each weight tile.
+constexpr int kDefaultCluster = 2;
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ---------------------------------------------------------------- launch helpers
-template <int KIND, int BN, int CG, bool SPLIT3>
-int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid, cudaStream_t s) {
+// Persistent launch: grid = as many CTAs (clusters of CL) as can be co-resident,
+// capped by the work.  Clusters of 4 cannot use every SM (GPC granularity), so
+// the co-resident count comes from cudaOccupancyMaxActiveClusters.
+template <int KIND, int BN, int CG, bool SPLIT3, int CL>
+int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_ctas, cudaStream_t s) {
     using L = pdl::Smem<KIND, BN, CG, SPLIT3>;
-    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3>;
+    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
+    static int max_ctas = 0;
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.blockDim = dim3(pdl::kThreads);
+    lc.dynamicSmemBytes = L::TOTAL;
+    lc.stream = s;
+    lc.attrs = at;
+    lc.numAttrs = 1;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        if (attr_err != cudaSuccess) return;
+        int ncl = 0;
+        lc.gridDim = dim3(CL * 64);
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &lc) != cudaSuccess || ncl <= 0)
+            ncl = sm_count / CL;
+        cudaGetLastError();
+        max_ctas = std::min(ncl * CL, sm_count / CL * CL);
     });
     if (attr_err != cudaSuccess)
         return fail(PDL_ELAUNCH, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-    kern<<<grid, pdl::kThreads, L::TOTAL, s>>>(maps, p);
+    int grid = std::min(max_ctas, (work_ctas + CL - 1) / CL * CL);
+    if (KIND == pdl::KIND_STEM) grid = std::max(p.n_tiles, grid / p.n_tiles * p.n_tiles);
+    lc.gridDim = dim3(grid);
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, p);
+    if (e != cudaSuccess) return fail(PDL_ELAUNCH, "tile_mma_kernel launch: %s", cudaGetErrorString(e));
     ++g_launches;
     return check_launch("tile_mma_kernel");
 }
 
-template <int KIND, bool SPLIT3>
-int dispatch_tile(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, dim3 grid,
-                  cudaStream_t s) {
-    if constexpr (KIND == pdl::KIND_GEMM || KIND == pdl::KIND_STEM) {
+template <int KIND, bool SPLIT3, int CL>
+int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, int work,
+                cudaStream_t s) {
+    if constexpr (KIND == pdl::KIND_STEM) {
+        if (bn == 64 && CL == 1) return launch_tile<KIND, 64, 1, SPLIT3, 1>(maps, p, work, s);
+    } else if constexpr (KIND == pdl::KIND_GEMM) {
         switch (bn) {
-            case 64: return launch_tile<KIND, 64, 1, SPLIT3>(maps, p, grid, s);
-            case 128: return launch_tile<KIND, 128, 1, SPLIT3>(maps, p, grid, s);
+            case 64: return launch_tile<KIND, 64, 1, SPLIT3, CL>(maps, p, work, s);
+            case 128: return launch_tile<KIND, 128, 1, SPLIT3, CL>(maps, p, work, s);
         }
     } else {
-        if (bn == 64 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3>(maps, p, grid, s);
-        if (bn == 64 && cg == 2) return launch_tile<KIND, 64, 2, SPLIT3>(maps, p, grid, s);
-        if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3>(maps, p, grid, s);
-        if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3>(maps, p, grid, s);
-        if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3>(maps, p, grid, s);
+        if (bn == 64 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3, CL>(maps, p, work, s);
+        if (bn == 64 && cg == 2) return launch_tile<KIND, 64, 2, SPLIT3, CL>(maps, p, work, s);
+        if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3, CL>(maps, p, work, s);
+        if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3, CL>(maps, p, work, s);
+        if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, CL>(maps, p, work, s);
     }
-    return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d", bn, cg);
+    return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
+}
+
+template <int KIND, bool SPLIT3>
+int dispatch_tile(int bn, int cg, int cl, const pdl::TmaMaps &maps, const pdl::TileParams &p,
+                  cudaStream_t s) {
+    // work in CTAs: one per (M-tile, N-tile), rounded up to whole clusters per N-tile
+    const int work = ((p.m_tiles + cl - 1) / cl) * cl * p.n_tiles;
+    if constexpr (KIND == pdl::KIND_STEM) return dispatch_bn<KIND, SPLIT3, 1>(bn, cg, maps, p, work, s);
+    else {
+        switch (cl) {
+            case 1: return dispatch_bn<KIND, SPLIT3, 1>(bn, cg, maps, p, work, s);
+            case 2: return dispatch_bn<KIND, SPLIT3, 2>(bn, cg, maps, p, work, s);
+            case 4: return dispatch_bn<KIND, SPLIT3, 4>(bn, cg, maps, p, work, s);
+        }
+    }
+    return fail(PDL_EUNSUPPORTED, "cluster size %d not in {1,2,4}", cl);
 }
 
 // ---------------------------------------------------------------- conv geometry
@@ -153,9 +200,15 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad) {
 }
 
 // Narrow-channel path (ResNet stem): <= 4 real input channels, <= 8 taps per row.
-bool is_stem(int C, int S, int stride) { return C <= 4 && S <= 8 && (stride == 1 || stride == 2); }
+bool is_stem(int C, int R, int S, int stride) {
+    return C <= 4 && S <= 8 && R <= pdl::kStemMaxR && (stride == 1 || stride == 2);
+}
 
 int ceil16(int c) { return (c + 15) / 16; }
+
+// Input channels per packed weight row: 32 (128-byte SW128 rows) when the number
+// of 16-channel blocks is even, else 16 (64-byte SW64 rows).
+int weight_group(int C) { return ceil16(C) % 2 == 0 ? 32 : 16; }
 
 void conv_default_cfg(int C, int K, pdl_tile_cfg *c) {
     const int CT = ceil16(C);
@@ -164,7 +217,8 @@ void conv_default_cfg(int C, int K, pdl_tile_cfg *c) {
     int cg = (CT % 2 == 0) ? 2 : 1;
     c->bk = 16 * cg;
     c->stages = 0;
-    c->cluster_m = c->cluster_n = c->split_k = 1;
+    c->cluster_m = kDefaultCluster;
+    c->cluster_n = c->split_k = 1;
     c->raster = 0;
 }
 
@@ -185,7 +239,8 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
                   const pdl_tile_cfg *cfg_in, cudaStream_t st) {
     int rc;
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
-    const int bn = (cfg_in && cfg_in->bn) ? cfg_in->bn : (K % 128 == 0 ? 128 : 64);
+    const int bn = 64;  // resident weights: 2 planes x 7 rows x 8 taps x 64 x 16 B = 112 KB
+    (void)cfg_in;
     const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
     const int BW = std::min({Q, 128, (256 - S) / stride + 1});
     const int box_w = (BW - 1) * stride + S;
@@ -195,7 +250,9 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
         const cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
         const cuuint64_t str[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
         const cuuint32_t box[5] = {4, (cuuint32_t)box_w, 1, 1, 1};
-        if ((rc = encode(&maps.a[0], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem x")))
+        // only 16 of every 64 bytes are used: do not promote to 256B L2 fills
+        if ((rc = encode(&maps.a[0], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem x",
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE)))
             return rc;
     }
     {
@@ -203,7 +260,7 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
         const cuuint64_t dims[5] = {4, (cuuint64_t)K, 8, (cuuint64_t)R, (cuuint64_t)planes};
         const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)8 * K * 16,
                                    (cuuint64_t)R * 8 * K * 16};
-        const cuuint32_t box[5] = {4, (cuuint32_t)bn, 8, 1, (cuuint32_t)planes};
+        const cuuint32_t box[5] = {4, (cuuint32_t)bn, 8, (cuuint32_t)R, 1};  // one plane, resident
         if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
             return rc;
     }
@@ -231,9 +288,9 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     p.tiles_h = P;
     p.m_tiles = p.tiles_w * P * N;
     p.n_tiles = (K + bn - 1) / bn;
-    dim3 grid(std::min(p.m_tiles * p.n_tiles, sm_count));
-    if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, 1, maps, p, grid, st);
-    return dispatch_tile<pdl::KIND_STEM, false>(bn, 1, maps, p, grid, st);
+    // the grid is a multiple of n_tiles: every CTA keeps one N-tile (resident weights)
+    if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, 1, 1, maps, p, st);
+    return dispatch_tile<pdl::KIND_STEM, false>(bn, 1, 1, maps, p, st);
 }
 
 int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, int N, int C, int K,
@@ -242,7 +299,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     int rc;
     if ((rc = get_encode())) return rc;
     if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
-    if (is_stem(C, S, stride))
+    if (is_stem(C, R, S, stride))
         return conv_fwd_stem(x, wp, bias, y, N, C, K, H, W, R, S, stride, pad, flags, cfg_in, st);
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
@@ -250,9 +307,14 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     if (cfg_in) {
         if (cfg_in->bn) cfg.bn = cfg_in->bn;
         if (cfg_in->bk) cfg.bk = cfg_in->bk;
+        if (cfg_in->cluster_m) cfg.cluster_m = cfg_in->cluster_m;
         cfg.raster = cfg_in->raster;
     }
-    const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16;
+    const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16, cl = cfg.cluster_m;
+    const int G = weight_group(C);
+    if ((G == 32) != (cg >= 2)) return fail(PDL_EINVAL, "conv: bk=%d incompatible with C=%d", cfg.bk, C);
+    if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "conv: cluster_m must be 1, 2 or 4");
+    if (cfg.bn % (8 * cl)) return fail(PDL_EINVAL, "conv: bn=%d not divisible into %d slices", cfg.bn, cl);
     if (cg < 1 || CT % cg) return fail(PDL_EINVAL, "conv: bk=%d does not divide C=%d", cfg.bk, C);
     const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad);
 
@@ -281,11 +343,17 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     }
     {
         const int planes = split ? 2 : 1;
-        const cuuint64_t dims[5] = {16, (cuuint64_t)K, (cuuint64_t)(R * S), (cuuint64_t)CT, (cuuint64_t)planes};
-        const cuuint64_t str[4] = {64, (cuuint64_t)K * 64, (cuuint64_t)R * S * K * 64,
-                                   (cuuint64_t)CT * R * S * K * 64};
-        const cuuint32_t bbox[5] = {16, (cuuint32_t)cfg.bn, 1, (cuuint32_t)cg, (cuuint32_t)planes};
-        if ((rc = encode(&maps.b, wp, 5, dims, str, bbox, CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
+        const int NB = cg >= 2 ? cg / 2 : 1;
+        const cuuint64_t rowb = (cuuint64_t)G * 4;
+        const cuuint64_t dims[5] = {(cuuint64_t)G, (cuuint64_t)K, (cuuint64_t)(R * S),
+                                    (cuuint64_t)(CT * 16 / G), (cuuint64_t)planes};
+        const cuuint64_t str[4] = {rowb, (cuuint64_t)K * rowb, (cuuint64_t)R * S * K * rowb,
+                                   (cuuint64_t)(CT * 16 / G) * R * S * K * rowb};
+        // cluster: each CTA multicasts a BN/cl-row slice of one (plane, nb) sub-tile per op
+        const cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(cfg.bn / cl), 1,
+                                    (cuuint32_t)(cl == 1 ? NB : 1), (cuuint32_t)(cl == 1 ? planes : 1)};
+        if ((rc = encode(&maps.b, wp, 5, dims, str, bbox,
+                         G == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
             return rc;
     }
     pdl::TileParams p{};
@@ -312,9 +380,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
     p.raster = cfg.raster;
     p.n_tiles = (K + cfg.bn - 1) / cfg.bn;
-    dim3 grid(std::min(p.m_tiles * p.n_tiles, sm_count));
-    if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, maps, p, grid, st);
-    return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, maps, p, grid, st);
+    if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, cl, maps, p, st);
+    return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, cl, maps, p, st);
 }
 
 }  // namespace
@@ -328,7 +395,7 @@ int pdl_device_check(void) { return device_check(); }
 
 size_t pdl_conv2d_packed_bytes(int C, int K, int R, int S, unsigned flags) {
     const int planes = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 ? 2 : 1;
-    if (is_stem(C, S, 1)) return (size_t)planes * R * 8 * K * 4 * sizeof(float);
+    if (is_stem(C, R, S, 1)) return (size_t)planes * R * 8 * K * 4 * sizeof(float);
     return (size_t)planes * ceil16(C) * 16 * K * R * S * sizeof(float);
 }
 
@@ -340,7 +407,7 @@ int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R
     if (C <= 0 || K % 16 || K <= 0 || R <= 0 || S <= 0) return fail(PDL_EINVAL, "prepack: bad shape");
     if (!aligned16(w) || !aligned16(packed)) return fail(PDL_EALIGN, "prepack: unaligned pointer");
     const int split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
-    if (is_stem(C, S, 1)) {
+    if (is_stem(C, R, S, 1)) {
         const long long plane = (long long)R * 8 * K * 4;
         const int blocks = (int)std::min<long long>((plane + 255) / 256, 148LL * 16);
         pdl::prepack_stem_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
@@ -349,7 +416,8 @@ int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R
         const long long total = (long long)K * ceil16(C) * 16 * R * S;
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
         pdl::prepack_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-            w, reinterpret_cast<float *>(packed), ceil16(C), K / 16, R * S, split, C);
+            w, reinterpret_cast<float *>(packed), ceil16(C), K / 16, R * S, split, C,
+            weight_group(C));
     }
     ++g_launches;
     return check_launch("prepack_weights_kernel");
@@ -426,11 +494,13 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     }
     if ((rc = get_encode())) return rc;
     int bn = N <= 64 ? 64 : 128;
-    int raster = 0;
+    int raster = 0, cl = kDefaultCluster;
     if (cfg_in) {
         if (cfg_in->bn) bn = cfg_in->bn;
+        if (cfg_in->cluster_m) cl = cfg_in->cluster_m;
         raster = cfg_in->raster;
     }
+    if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "gemm: cluster_m must be 1, 2 or 4");
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     {
@@ -459,9 +529,8 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     p.raster = raster;
     p.m_tiles = (M + 127) / 128;
     p.n_tiles = (N + bn - 1) / bn;
-    dim3 grid(std::min(p.m_tiles * p.n_tiles, sm_count));
-    if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, maps, p, grid, st);
-    return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, maps, p, grid, st);
+    if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, cl, maps, p, st);
+    return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, cl, maps, p, st);
 }
 
 int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int Q, unsigned flags,
@@ -502,7 +571,8 @@ int pdl_default_cfg(int op, const int *dims, pdl_tile_cfg *cfg) {
         cfg->bn = dims[1] <= 64 ? 64 : 128;
         cfg->bk = 32;
         cfg->stages = 0;
-        cfg->cluster_m = cfg->cluster_n = cfg->split_k = 1;
+        cfg->cluster_m = kDefaultCluster;
+        cfg->cluster_n = cfg->split_k = 1;
         cfg->raster = 0;
         return PDL_OK;
     }

@@ -31,6 +31,14 @@ namespace pdl {
 
 enum { KIND_GEMM = 0, KIND_CONV = 1, KIND_STEM = 2 };
 
+// Diagnostic switches (flags bits >= 8, never set by the public API wrappers):
+// results are WRONG when set; used only to attribute time between pipeline roles.
+enum : unsigned {
+    DBG_NO_A_TMA = 1u << 8,     // producer skips the A loads
+    DBG_NO_STAGE_ST = 1u << 9,  // staging warps skip the tcgen05.st into TMEM
+    DBG_NO_EPI_STORE = 1u << 10  // epilogue skips the global stores
+};
+
 // Geometry / epilogue parameters (by value, param space).
 struct TileParams {
     // common
@@ -60,40 +68,58 @@ struct TmaMaps {
 
 // Shared-memory tiles of one pipeline stage.
 //   GEMM: A [128 rows][32 fp32]   SW128 K-major        B [BN/32][32 k][32 n] SW128_B32 MN-major
-//   CONV: A [CG][128 rows][16]    SW64  K-major        B [CG][BN rows][16]   SW64 K-major
-//   STEM: A [256 px][4 fp32]      halo row, no swizzle B [8 taps][BN][4]     no swizzle K-major
+//   CONV: A [CG][128 rows][16]    SW64  K-major        B [CG/2][BN rows][32] SW128 K-major
+//                                                      (CG = 1: B [BN rows][16] SW64)
+//   STEM: A [256 px][4 fp32]      halo row, no swizzle B resident: [plane][R][8 taps][BN][4]
 template <int KIND, int BN, int CG>
 struct Geo {
     static constexpr int BM = 128;
     static constexpr int A_SUB = KIND == KIND_GEMM ? BM * 128 : KIND == KIND_CONV ? BM * 64 : 4096;
-    static constexpr int B_SUB = KIND == KIND_GEMM ? BN * 128 : KIND == KIND_CONV ? BN * 64 : BN * 128;
+    // conv weights: 128-byte rows (32 input channels, SW128) whenever CG >= 2 -- 64-byte
+    // SW64 rows make every tensor-core B read 2-way bank conflicted
+    static constexpr int B_ROW = (KIND == KIND_CONV && CG == 1) ? 64 : 128;
+    static constexpr int NB = KIND == KIND_CONV ? (CG >= 2 ? CG / 2 : 1) : 1;
+    static constexpr int B_SUB = KIND == KIND_STEM ? BN * 128 : BN * B_ROW;
     static constexpr int NSUB = KIND == KIND_CONV ? CG : 1;
     static constexpr int A_BYTES = A_SUB * NSUB;
-    static constexpr int B_BYTES = B_SUB * NSUB;
+    static constexpr int B_BYTES = B_SUB * NB;
     static constexpr int KK = KIND == KIND_CONV ? 2 : 4;  // K=8 MMAs per sub-tile
     static constexpr int KS = KIND == KIND_CONV ? 16 * CG : 32;  // K elements per stage
 };
 
+constexpr int kStemMaxR = 7;  // resident stem weights: R <= 7 kernel rows
+
 // TS = A operand staged in TMEM by the split warps (3xTF32, and the stem's tap gather).
+// SMEM stages (TMA ring) and TMEM A slots (split -> MMA ring) are separate rings.
 template <int KIND, int BN, int CG, bool SPLIT3>
 struct Smem {
     using G = Geo<KIND, BN, CG>;
     static constexpr bool TS = SPLIT3 || KIND == KIND_STEM;
-    static constexpr int STAGE = G::A_BYTES + G::B_BYTES * (SPLIT3 ? 2 : 1);
-    static constexpr int BUDGET = 216 * 1024;
+    static constexpr int PLANES = SPLIT3 ? 2 : 1;  // B planes resident in a stage (hi, lo)
+    // B planes loaded by TMA: conv / stem weights carry both (prepacked once); the
+    // GEMM loads B itself and the staging warps form lo = B - tf32(B) in smem.
+    // (Forming the conv weights' lo on chip too was measured 5-12% slower: the
+    // staging warps' smem traffic costs more than the TMA bytes it saves.)
+    static constexpr int LOAD_PLANES = KIND == KIND_GEMM ? 1 : PLANES;
+    // stem weights stay resident for the whole kernel (one N-tile per CTA)
+    static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * kStemMaxR * 8 * BN * 16 : 0;
+    static constexpr int STAGE = KIND == KIND_STEM ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
+    static constexpr int BUDGET = 216 * 1024 - W_BYTES;
+    static constexpr int S0 = BUDGET / STAGE;
+    static constexpr int STAGES = S0 > 16 ? 16 : S0;
     static constexpr int SLOT_COLS = SPLIT3 ? 2 * G::KS : G::KS;  // TMEM columns per A slot
     static constexpr int A_SLOT0 = 2 * BN;                        // after the 2 accumulators
-    static constexpr int S_SMEM = BUDGET / STAGE;
-    static constexpr int S_TMEM = TS ? (512 - A_SLOT0) / SLOT_COLS : 8;
-    static constexpr int S0 = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
-    static constexpr int STAGES = S0 > 8 ? 8 : S0;
+    static constexpr int T0 = TS ? (512 - A_SLOT0) / SLOT_COLS : 1;
+    static constexpr int TSLOTS = T0 > 8 ? 8 : T0;
     static constexpr int A_OFF = 0;
     static constexpr int B_HI = G::A_BYTES;
     static constexpr int B_LO = B_HI + G::B_BYTES;
-    static constexpr int BAR_OFF = STAGES * STAGE;
-    static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + alignment slack
+    static constexpr int W_OFF = STAGES * STAGE;       // stem weights
+    static constexpr int BAR_OFF = W_OFF + W_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 1024 + 1024;  // barriers + alignment slack
     static constexpr uint32_t TMEM_COLS = TS ? 512 : 2 * BN;
     static_assert(STAGES >= 2, "tile too large for a 2-stage pipeline");
+    static_assert(!TS || TSLOTS >= 2, "not enough TMEM for two A slots");
 };
 
 __device__ __forceinline__ float tf32_lo(float x) {
@@ -102,16 +128,27 @@ __device__ __forceinline__ float tf32_lo(float x) {
     return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t saddr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(saddr));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t saddr, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
 // lo = x - tf32(x) for `bytes` of shared memory (element-wise, layout-agnostic).
-__device__ __forceinline__ void split_lo_smem(const uint8_t *src, uint8_t *lo, int bytes, int tid,
+__device__ __forceinline__ void split_lo_smem(uint32_t src, uint32_t lo, int bytes, int tid,
                                               int nthreads) {
-    const float4 *s4 = reinterpret_cast<const float4 *>(src);
-    float4 *l4 = reinterpret_cast<float4 *>(lo);
     const int n = bytes >> 4;
 #pragma unroll 4
     for (int i = tid; i < n; i += nthreads) {
-        const float4 v = s4[i];
-        l4[i] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+        const float4 v = lds128(src + i * 16);
+        sts128(lo + i * 16, make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w)));
     }
 }
 
@@ -148,18 +185,22 @@ __device__ __forceinline__ void store16(const TileParams &p, float *dst, int col
     }
 }
 
-// Persistent implicit-GEMM tile engine.  gridDim.x CTAs (<= #SMs), one per SM;
-// CTA b processes tiles b, b + gridDim.x, ... (N-tiles fastest so concurrent
-// CTAs share activation rows through L2).
+// Persistent implicit-GEMM tile engine.  gridDim.x CTAs (<= #SMs, a multiple of
+// the N-tile count so every CTA keeps one N-tile), one per SM; CTA b processes
+// tiles b, b + gridDim.x, ... (N-tiles fastest: concurrent CTAs share
+// activation rows through L2).
 //   warp 0       TMA producer (one lane), runs ahead across tile boundaries
 //   warp 1       tcgen05.mma issuer (one lane)
 //   warp 2       TMEM allocator
 //   warps 4-7    A staging (TS modes): thread = tile row = TMEM lane; reads its
-//                row of the landed tile (conv: gathers the stem's taps), writes
-//                hi (= x, the tensor core truncates) and lo = x - tf32(x) into a
-//                TMEM A slot with tcgen05.st; GEMM also forms B's lo in smem
+//                row of the landed tile (stem: gathers the taps), writes hi (= x,
+//                the tensor core truncates) and lo = x - tf32(x) into a TMEM A
+//                slot with tcgen05.st; the GEMM also forms B's lo in smem
 //   warps 8-15   TMEM drain + epilogue; warp 8+e owns TMEM lanes 32*(e%4).. and
 //                output columns [(e/4)*BN/2, (e/4+1)*BN/2)
+// Rings: SMEM stages  full[s] (TMA -> staging) / empty[s] (staging [+ MMA] -> TMA);
+//        TMEM A slots tready[t] (staging -> MMA) / tfree[t] (MMA -> staging);
+//        accumulators tmem_full[b] (MMA -> epilogue) / tmem_empty[b] (epilogue -> MMA).
 // 3xTF32 issues hi*hi + hi*lo + lo*hi per K=8 step.  The reduction of every tile
 // is cut into segments of p.seg_kb k-blocks; each segment accumulates in one of
 // two TMEM buffers (ping-pong, continuing across tiles) and is drained into
@@ -202,28 +243,44 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     return c;
 }
 
-template <int KIND, int BN, int CG, bool SPLIT3>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
+    static_assert(CL == 1 || KIND != KIND_STEM, "the stem keeps its weights resident");
     using G = Geo<KIND, BN, CG>;
     using L = Smem<KIND, BN, CG, SPLIT3>;
     constexpr bool TS = L::TS;
     constexpr int STAGES = L::STAGES;
+    constexpr int TSLOTS = L::TSLOTS;
     constexpr int HALF = BN / 2;  // columns per epilogue warp
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem =
         reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);
-    uint64_t *ready = full + STAGES;
-    uint64_t *empty = ready + STAGES;
-    uint64_t *tmem_full = empty + STAGES;  // [2]
+    uint64_t *empty = full + STAGES;
+    uint64_t *tready = empty + STAGES;
+    uint64_t *tfree = tready + 8;
+    uint64_t *tmem_full = tfree + 8;       // [2]
     uint64_t *tmem_empty = tmem_full + 2;  // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+    uint64_t *wfull = tmem_empty + 2;      // stem weights landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int num_tiles = p.m_tiles * p.n_tiles;
     const int seg_kb = p.seg_kb;
+    // Cluster of CL CTAs = CL consecutive M-tiles of one N-tile ("super-tile"),
+    // processed in lockstep; each CTA loads 1/CL of the B tile and multicasts it.
+    const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+    const int cid = blockIdx.x / CL;
+    const int ncl = gridDim.x / CL;
+    const int num_super = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
+    const uint16_t cl_mask = (uint16_t)((1u << CL) - 1);
+    auto tile_of = [&](int st) {  // M-tile may exceed m_tiles (phantom: loads OOB zeros, stores masked)
+        const int mg = st / p.n_tiles;
+        const int nt = st - mg * p.n_tiles;
+        return (mg * CL + rank) * p.n_tiles + nt;
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&maps.b);
@@ -233,22 +290,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_prefetch(&maps.a[2]);
             tma_prefetch(&maps.a[3]);
         }
+        // stem: only the staging warps read a stage; conv/GEMM: staging (A) + the MMA
+        // commits of all CL CTAs (B is multicast into every CTA of the cluster)
+        const uint32_t empty_count = KIND == KIND_STEM ? 128 : (TS ? 128 : 0) + CL;
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&ready[s], 128);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], empty_count);
+        }
+        for (int t = 0; t < TSLOTS; ++t) {
+            mbar_init(&tready[t], 128);
+            mbar_init(&tfree[t], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full[b], 1);
             mbar_init(&tmem_empty[b], kEpiThreads);
         }
+        mbar_init(wfull, 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<L::TMEM_COLS>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    if (CL > 1) cluster_sync();  // peers multicast into our barriers: they must exist
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t smem0 = smem_u32(smem);
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -256,22 +322,35 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t tx;
             if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
             else if (KIND == KIND_CONV)
-                tx = (uint32_t)(CG * 64 * p.BW * p.BH * p.BNI + CG * BN * 64 * (SPLIT3 ? 2 : 1));
-            else tx = (uint32_t)(16 * p.box_w + BN * 128 * (SPLIT3 ? 2 : 1));
+                tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
+                                G::B_BYTES * L::LOAD_PLANES);
+            else tx = (uint32_t)(16 * p.box_w);
+            if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
+                // resident weights of this CTA's N-tile: [plane][R][8 taps][BN][4]
+                const int n0 = (blockIdx.x % p.n_tiles) * BN;
+                mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.R * 8 * BN * 16));
+                for (int pl = 0; pl < L::PLANES; ++pl)
+                    tma_load_5d(smem + L::W_OFF + pl * (kStemMaxR * 8 * BN * 16), &maps.b, wfull, 0,
+                                n0, 0, 0, pl);
+            }
             int s = 0;
             uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const TileCoord tc = tile_coord<KIND, BN>(p, tile);
+            for (int st = cid; st < num_super; st += ncl) {
+                const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t *st = smem + s * L::STAGE;
+                    uint8_t *sp = smem + s * L::STAGE;
                     mbar_arrive_expect_tx(&full[s], tx);
                     if (KIND == KIND_GEMM) {
-                        tma_load_2d(st + L::A_OFF, &maps.a[0], &full[s], kb * 32, tc.m0);
-#pragma unroll
-                        for (int c = 0; c < BN / 32; ++c)
-                            tma_load_2d(st + L::B_HI + c * 4096, &maps.b, &full[s], tc.n0 + c * 32,
-                                        kb * 32);
+                        tma_load_2d(sp + L::A_OFF, &maps.a[0], &full[s], kb * 32, tc.m0);
+                        for (int c = rank; c < BN / 32; c += CL) {
+                            if (CL == 1)
+                                tma_load_2d(sp + L::B_HI + c * 4096, &maps.b, &full[s],
+                                            tc.n0 + c * 32, kb * 32);
+                            else
+                                tma_load_2d_mc(sp + L::B_HI + c * 4096, &maps.b, &full[s],
+                                               tc.n0 + c * 32, kb * 32, cl_mask);
+                        }
                     } else if (KIND == KIND_CONV) {
                         const int rs_n = p.R * p.S;
                         const int ctg = kb / rs_n;
@@ -285,16 +364,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                             dh = (dh - ph2) >> 1;
                             dw = (dw - pw2) >> 1;
                         }
+                        if (!(p.flags & DBG_NO_A_TMA)) {
 #pragma unroll
-                        for (int c = 0; c < CG; ++c)
-                            tma_load_5d(st + L::A_OFF + c * G::A_SUB, &maps.a[mi], &full[s], 0,
-                                        tc.q0 + dw, tc.p0 + dh, ctg * CG + c, tc.i0);
-                        tma_load_5d(st + L::B_HI, &maps.b, &full[s], 0, tc.n0, rs, ctg * CG, 0);
+                            for (int c = 0; c < CG; ++c)
+                                tma_load_5d(sp + L::A_OFF + c * G::A_SUB, &maps.a[mi], &full[s], 0,
+                                            tc.q0 + dw, tc.p0 + dh, ctg * CG + c, tc.i0);
+                        }
+                        if (CL == 1) {
+                            tma_load_5d(sp + L::B_HI, &maps.b, &full[s], 0, tc.n0, rs, ctg * G::NB, 0);
+                        } else {
+                            // this CTA's slice: rows [rank*BN/CL, +BN/CL) of every (plane, nb) sub-tile
+                            constexpr int SL = BN / CL;
+#pragma unroll
+                            for (int pl = 0; pl < L::LOAD_PLANES; ++pl)
+#pragma unroll
+                                for (int nb = 0; nb < G::NB; ++nb)
+                                    tma_load_5d_mc(sp + L::B_HI + pl * G::B_BYTES + nb * G::B_SUB +
+                                                       rank * SL * G::B_ROW,
+                                                   &maps.b, &full[s], 0, tc.n0 + rank * SL, rs,
+                                                   ctg * G::NB + nb, pl, cl_mask);
+                        }
                     } else {
                         // stem: k-block = kernel row r; one halo row of 4-channel pixels
-                        tma_load_5d(st + L::A_OFF, &maps.a[0], &full[s], 0,
+                        tma_load_5d(sp + L::A_OFF, &maps.a[0], &full[s], 0,
                                     tc.q0 * p.stride - p.pad, tc.p0 * p.stride + kb - p.pad, 0, tc.i0);
-                        tma_load_5d(st + L::B_HI, &maps.b, &full[s], 0, tc.n0, 0, kb, 0);
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
@@ -304,11 +397,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== MMA issuer (one thread) =====================
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(128, BN, KIND == KIND_GEMM ? 1 : 0);
-            const uint32_t smem0 = smem_u32(smem);
-            int s = 0;
-            uint32_t ph = 0;
+            if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
+                mbar_wait(wfull, 0);
+                tc_fence_after();
+            }
+            int s = 0, t = 0;
+            uint32_t ph = 0, tph = 0;
             int g = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int st_i = cid; st_i < num_super; st_i += ncl) {
                 int in_seg = 0;
                 uint32_t d_tmem = tmem_base;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -317,10 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tc_fence_after();
                         d_tmem = tmem_base + (uint32_t)((g & 1) * BN);
                     }
-                    mbar_wait(TS ? &ready[s] : &full[s], ph);
+                    if (TS) mbar_wait(&tready[t], tph);
+                    else mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t st = smem0 + s * L::STAGE;
-                    const uint32_t a_t = tmem_base + L::A_SLOT0 + s * L::SLOT_COLS;
+                    const uint32_t a_t = tmem_base + L::A_SLOT0 + t * L::SLOT_COLS;
 #pragma unroll
                     for (int c = 0; c < G::NSUB; ++c) {
 #pragma unroll
@@ -333,15 +430,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 bhi = smem_desc(st + L::B_HI + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
                                 blo = smem_desc(st + L::B_LO + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
                             } else if (KIND == KIND_CONV) {
-                                const uint32_t b_off = c * G::B_SUB + kk * 32;
-                                bhi = smem_desc(st + L::B_HI + b_off, 16, 512, LAYOUT_SW64);
-                                blo = smem_desc(st + L::B_LO + b_off, 16, 512, LAYOUT_SW64);
+                                const uint32_t kbyte = (c * G::KK + kk) * 32;  // K=8 step -> 32 B
+                                const uint32_t b_off = (kbyte / G::B_ROW) * G::B_SUB + kbyte % G::B_ROW;
+                                const uint32_t lay = G::B_ROW == 128 ? LAYOUT_SW128 : LAYOUT_SW64;
+                                bhi = smem_desc(st + L::B_HI + b_off, 16, 8 * G::B_ROW, lay);
+                                blo = smem_desc(st + L::B_LO + b_off, 16, 8 * G::B_ROW, lay);
                             } else {
-                                // no-swizzle K-major: 8-row x 16B core matrices; taps
-                                // (2kk, 2kk+1) are two core-matrix columns BN*16 B apart
-                                const uint32_t b_off = kk * 2 * BN * 16;
-                                bhi = smem_desc(st + L::B_HI + b_off, BN * 16, 128, 0);
-                                blo = smem_desc(st + L::B_LO + b_off, BN * 16, 128, 0);
+                                // resident no-swizzle K-major weights: 8-row x 16B core
+                                // matrices; taps (2kk, 2kk+1) are BN*16 B apart
+                                const uint32_t w = smem0 + L::W_OFF + (uint32_t)((kb * 8 + kk * 2) * BN * 16);
+                                bhi = smem_desc(w, BN * 16, 128, 0);
+                                blo = smem_desc(w + kStemMaxR * 8 * BN * 16, BN * 16, 128, 0);
                             }
                             const uint32_t acc = (in_seg | c | kk) != 0;
                             if (TS) {
@@ -360,8 +459,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    mma_commit(&empty[s]);
+                    if (KIND != KIND_STEM) {  // B (and SS-mode A) consumed, in every CTA
+                        if (CL == 1) mma_commit(&empty[s]);
+                        else mma_commit_mc(&empty[s], cl_mask);
+                    }
+                    if (TS) mma_commit(&tfree[t]);                 // A slot consumed
                     if (++s == STAGES) { s = 0; ph ^= 1; }
+                    if (++t == TSLOTS) { t = 0; tph ^= 1; }
                     if (++in_seg == seg_kb || kb + 1 == p.num_kb) {
                         mma_commit(&tmem_full[g & 1]);
                         in_seg = 0;
@@ -377,64 +481,84 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int quarter = warp - kSplitWarp0;
             const int row = quarter * 32 + lane;
             const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-            int s = 0;
-            uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            int s = 0, t = 0;
+            uint32_t ph = 0, tph = 0;
+            for (int st_i = cid; st_i < num_super; st_i += ncl) {
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(&full[s], ph);
-                    tc_fence_after();
-                    const uint8_t *sa = smem + s * L::STAGE + L::A_OFF;
-                    const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + s * L::SLOT_COLS;
+                    const uint32_t sa = smem0 + s * L::STAGE + L::A_OFF;
+                    const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + t * L::SLOT_COLS;
                     if (KIND == KIND_GEMM) {
                         float x[32], lo[32];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const float4 v = *reinterpret_cast<const float4 *>(
-                                sa + row * 128 + ((j ^ (row & 7)) << 4));
+                            const float4 v = lds128(sa + row * 128 + ((j ^ (row & 7)) << 4));
                             x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
                         }
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
-                        tmem_st32(t_hi, x);
-                        tmem_st32(t_hi + G::KS, lo);
-                        split_lo_smem(smem + s * L::STAGE + L::B_HI, smem + s * L::STAGE + L::B_LO,
+                        split_lo_smem(smem0 + s * L::STAGE + L::B_HI, smem0 + s * L::STAGE + L::B_LO,
                                       G::B_BYTES, tid, 128);
                         fence_proxy_async_smem();
-                    } else if (KIND == KIND_CONV) {
+                        mbar_arrive(&empty[s]);  // A rows read (B_lo written before MMA's commit)
 #pragma unroll
-                        for (int c = 0; c < CG; ++c) {
-                            float x[16], lo[16];
+                        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
+                        mbar_wait(&tfree[t], tph ^ 1);
+                        tc_fence_after();
+                        tmem_st32(t_hi, x);
+                        tmem_st32(t_hi + G::KS, lo);
+                    } else if (KIND == KIND_CONV) {
+                        float x[16 * CG];
+#pragma unroll
+                        for (int c = 0; c < CG; ++c)
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                const float4 v = *reinterpret_cast<const float4 *>(
-                                    sa + c * G::A_SUB + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
-                                x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+                                const float4 v =
+                                    lds128(sa + c * G::A_SUB + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
+                                x[16 * c + 4 * j] = v.x; x[16 * c + 4 * j + 1] = v.y;
+                                x[16 * c + 4 * j + 2] = v.z; x[16 * c + 4 * j + 3] = v.w;
                             }
+                        mbar_arrive(&empty[s]);  // A rows read
+                        mbar_wait(&tfree[t], tph ^ 1);
+                        tc_fence_after();
+                        if (!(p.flags & DBG_NO_STAGE_ST)) {
+                            // fully unrolled: x[] must stay in registers and the warp-collective
+                            // tcgen05.st must not sit in a data-dependent loop
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) lo[i] = tf32_lo(x[i]);
-                            tmem_st16(t_hi + c * 16, x);
-                            if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
+                            for (int c = 0; c < CG; ++c) {
+                                float hi[16], lo[16];
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    hi[i] = x[16 * c + i];
+                                    lo[i] = tf32_lo(hi[i]);
+                                }
+                                tmem_st16(t_hi + c * 16, hi);
+                                if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
+                            }
                         }
                     } else {
-                        // stem: gather taps s = 0..S-1 (4 channels each) of this output pixel
+                        // stem: gather taps 0..S-1 (4 channels each) of this output pixel
                         float x[32], lo[32];
                         const bool live = row < p.BW;
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) {
+                        for (int tp = 0; tp < 8; ++tp) {
                             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                            if (live && t < p.S)
-                                v = *reinterpret_cast<const float4 *>(sa + (row * p.stride + t) * 16);
-                            x[4 * t] = v.x; x[4 * t + 1] = v.y; x[4 * t + 2] = v.z; x[4 * t + 3] = v.w;
+                            if (live && tp < p.S) v = lds128(sa + (row * p.stride + tp) * 16);
+                            x[4 * tp] = v.x; x[4 * tp + 1] = v.y; x[4 * tp + 2] = v.z; x[4 * tp + 3] = v.w;
                         }
+                        mbar_arrive(&empty[s]);  // halo row read
 #pragma unroll
                         for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
-                        tmem_st32(t_hi, x);
-                        if (SPLIT3) tmem_st32(t_hi + G::KS, lo);
+                        mbar_wait(&tfree[t], tph ^ 1);
+                        tc_fence_after();
+                        if (!(p.flags & DBG_NO_STAGE_ST)) {
+                            tmem_st32(t_hi, x);
+                            if (SPLIT3) tmem_st32(t_hi + G::KS, lo);
+                        }
                     }
                     tmem_wait_st();
                     tc_fence_before();
-                    mbar_arrive(&ready[s]);
+                    mbar_arrive(&tready[t]);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
+                    if (++t == TSLOTS) { t = 0; tph ^= 1; }
                 }
             }
         }
@@ -447,21 +571,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
         int g = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const TileCoord tc = tile_coord<KIND, BN>(p, tile);
+        for (int st_i = cid; st_i < num_super; st_i += ncl) {
+            const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
             float sum[HALF];
-#pragma unroll
-            for (int i = 0; i < HALF; ++i) sum[i] = 0.f;
             for (int sg = 0; sg < nseg; ++sg, ++g) {
                 mbar_wait(&tmem_full[g & 1], (g >> 1) & 1);
                 tc_fence_after();
                 const uint32_t base = tmem_base + lane_off + (uint32_t)((g & 1) * BN + half * HALF);
+                if (sg == 0) {
+                    // first segment: load straight into the sums (all loads in flight, one wait)
 #pragma unroll
-                for (int j = 0; j < HALF / 16; ++j) {
-                    float v[16];
-                    tmem_ld16(base + j * 16, v);
+                    for (int j = 0; j < HALF / 16; ++j) tmem_ld16_nowait(base + j * 16, &sum[j * 16]);
+                    tmem_wait_ld();
+                } else {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) sum[j * 16 + i] += v[i];
+                    for (int j = 0; j < HALF / 32; ++j) {
+                        float v[32];
+                        tmem_ld16_nowait(base + j * 32, &v[0]);
+                        tmem_ld16_nowait(base + j * 32 + 16, &v[16]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) sum[j * 32 + i] += v[i];
+                    }
                 }
                 tc_fence_before();
                 mbar_arrive(&tmem_empty[g & 1]);
@@ -487,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ((size_t)(valid ? pp : 0) * p.Q + (valid ? qq : 0)) * 16;
                 cstride = plane;  // next 16-channel block kt
             }
-            if (valid) {
+            if (valid && !(p.flags & DBG_NO_EPI_STORE)) {
 #pragma unroll
                 for (int j = 0; j < HALF / 16; ++j) {
                     const int col0 = tc.n0 + half * HALF + j * 16;
@@ -502,7 +633,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     tc_fence_before();
-    __syncthreads();
+    if (CL > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<L::TMEM_COLS>(tmem_base);
@@ -629,13 +761,15 @@ __global__ void bias_relu_kernel(float4 *__restrict__ y, const float4 *__restric
     }
 }
 
-// Weight prepack KCRS16c16k -> packed[plane][ct][r*S+s][k][c] (K-major rows of
-// 16 input channels per output channel k); plane 0 = w (the tensor core
-// truncates to tf32), plane 1 = lo = w - tf32(w) for 3xTF32.  Input channels
-// >= C_real are zeroed (nChw16c pads C to a multiple of 16).
+// Weight prepack KCRS16c16k -> packed[plane][C/G][r*S+s][k][G] (K-major rows of G
+// input channels per output channel k; G = 32 when the channel-block count is
+// even, else 16); plane 0 = w (the tensor core truncates to tf32), plane 1 =
+// lo = w - tf32(w) for 3xTF32.  Input channels >= C_real are zeroed (nChw16c
+// pads C to a multiple of 16).
 __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__restrict__ out,
-                                       int CT, int KT, int RS, int split, int C_real) {
+                                       int CT, int KT, int RS, int split, int C_real, int G) {
     const long long total = (long long)KT * CT * RS * 256;
+    const int K = KT * 16;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         // source index order: kt, ct, rs, c, k
@@ -646,8 +780,9 @@ __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__res
         t /= RS;
         const int ct = t % CT;
         const int kt = (int)(t / CT);
-        const float v = (ct * 16 + c < C_real) ? w[i] : 0.f;
-        const size_t dst = ((((size_t)ct * RS + rs) * (KT * 16)) + (size_t)kt * 16 + k) * 16 + c;
+        const int cin = ct * 16 + c;
+        const float v = (cin < C_real) ? w[i] : 0.f;
+        const size_t dst = ((((size_t)(cin / G) * RS + rs) * K) + (size_t)kt * 16 + k) * G + cin % G;
         out[dst] = v;
         if (split) out[dst + total] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     }

@@ -208,6 +208,36 @@ def test_narrow_channel_stem(P, c, r, stride, h, mode):
     assert rel(y.cpu().numpy(), ref) <= TOL[mode]
 
 
+@pytest.mark.parametrize("cluster", [1, 2, 4])
+@pytest.mark.parametrize("layer", [l for l in W.LAYERS if l.idx in (3, 6, 7, 13, 17)],
+                         ids=lambda l: l.name())
+def test_cluster_multicast_conv(P, layer, cluster):
+    """Weight tiles multicast across clusters of 1/2/4 CTAs give identical results
+    (same reduction order per element) and match the oracle."""
+    x, w, b, ref = _conv_ref(layer, 2, True)
+    ys = []
+    for mode in ("3xtf32", "tf32"):
+        y = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=layer.stride, pad=layer.pad,
+                             relu=True, mode=mode, cfg={"cluster_m": cluster})
+        assert rel(y.cpu().numpy(), ref) <= TOL[mode]
+        ys.append(y)
+    y1 = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=layer.stride, pad=layer.pad,
+                          relu=True, cfg={"cluster_m": 1})
+    assert torch.equal(ys[0], y1)
+
+
+@pytest.mark.parametrize("cluster", [1, 2, 4])
+@pytest.mark.parametrize("shape", [(300, 192, 100), (1024, 1024, 1024), (49, 2048, 512)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_cluster_multicast_gemm(P, shape, cluster):
+    m, n, k = shape
+    a, b = W.gemm_inputs(m, n, k, seed=17)
+    ref = oracle.gemm_f64(a, b)
+    for mode in ("3xtf32", "tf32"):
+        c = P.gemm(cuda(a), cuda(b), mode=mode, cfg={"cluster_m": cluster}).cpu().numpy()
+        assert rel(c, ref) <= TOL[mode]
+
+
 def test_bad_shapes_raise(P):
     x = torch.zeros((1, 1, 4, 4, 16), device="cuda")
     w = torch.zeros((1, 1, 3, 3, 16, 16), device="cuda")
