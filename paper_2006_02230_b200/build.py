@@ -44,6 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(4, "-Xptxas=-v")
     if os.environ.get("PDL_WATCHDOG"):
         cmd.insert(4, "-DPDL_WATCHDOG=1")
+    if os.environ.get("PDL_TRACE"):
+        cmd.insert(4, "-DPDL_TRACE=1")
     env = dict(os.environ)
     if os.path.exists("/usr/bin/g++"):
         cmd[1:1] = ["-ccbin", "/usr/bin/g++"]

@@ -86,6 +86,9 @@ int device_check() {
     return PDL_OK;
 }
 
+// PDL_TRACE builds: device buffer receiving block 0's event stamps (see pdl_trace_buffer).
+unsigned long long *g_trace = nullptr;
+
 // Reduction elements accumulated in TMEM before an fp32 round-to-nearest drain.
 constexpr int kSegElems = 256;
 // CTAs per cluster sharing (multicasting) each weight tile.
@@ -130,7 +133,9 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
     int grid = std::min(max_ctas, (work_ctas + CL - 1) / CL * CL);
     if (KIND == pdl::KIND_STEM) grid = std::max(p.n_tiles, grid / p.n_tiles * p.n_tiles);
     lc.gridDim = dim3(grid);
-    cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, p);
+    pdl::TileParams pt = p;
+    pt.trace = g_trace;
+    cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, pt);
     if (e != cudaSuccess) return fail(PDL_ELAUNCH, "tile_mma_kernel launch: %s", cudaGetErrorString(e));
     ++g_launches;
     return check_launch("tile_mma_kernel");
@@ -389,6 +394,12 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
 extern "C" {
 
 int pdl_abi_version(void) { return PDL_ABI_VERSION; }
+
+// Diagnostics (not in pdl.h): route tile-engine timeline stamps of block 0 to a
+// caller-owned device buffer of TR_COUNT * 4096 uint64 (PDL_TRACE builds only).
+void pdl_debug_set_trace(void *dev_buffer) {
+    g_trace = reinterpret_cast<unsigned long long *>(dev_buffer);
+}
 const char *pdl_last_error(void) { return g_err.c_str(); }
 int pdl_last_launch_count(void) { return g_launches; }
 int pdl_device_check(void) { return device_check(); }

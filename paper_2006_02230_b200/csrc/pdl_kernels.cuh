@@ -59,7 +59,37 @@ struct TileParams {
     int n_tiles;           // number of N tiles
     int raster;            // reserved
     int seg_kb;            // k-blocks per TMEM accumulation segment
+    unsigned long long *trace;  // PDL_TRACE builds: per-event clock64 stamps of block 0
 };
+
+// Timeline tracing (PDL_TRACE builds only): block 0 stamps clock64 at each
+// pipeline hand-off; slot = event * kTraceN + index.
+constexpr int kTraceN = 4096;
+enum TraceEv {
+    TR_P_ISSUE = 0,   // producer: stage free, issuing TMA for k-block i
+    TR_S_FULL,        // staging: data of k-block i landed
+    TR_S_TFREE,       // staging: TMEM slot free
+    TR_S_DONE,        // staging: A slot ready (tready arrived)
+    TR_M_READY,       // MMA: k-block i ready
+    TR_M_ISSUED,      // MMA: k-block i issued + committed
+    TR_E_FULL,        // epilogue: segment g landed in TMEM
+    TR_E_DRAINED,     // epilogue: segment g drained
+    TR_E_STORED,      // epilogue: tile j stored
+    TR_M_WAITED,      // MMA: barrier observed (before tcgen05.fence::after_thread_sync)
+    TR_M_LOOP,        // MMA: top of k-block loop
+    TR_COUNT
+};
+__device__ __forceinline__ void trace_ev(const TileParams &p, int ev, int i) {
+#ifdef PDL_TRACE
+    if (p.trace && blockIdx.x == 0 && i < kTraceN) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+        p.trace[ev * kTraceN + i] = t;
+    }
+#else
+    (void)p; (void)ev; (void)i;
+#endif
+}
 
 struct TmaMaps {
     CUtensorMap a[4];  // conv: one per (row, col) parity for stride 2; GEMM / stem: a[0]
@@ -85,6 +115,13 @@ struct Geo {
     static constexpr int B_BYTES = B_SUB * NB;
     static constexpr int KK = KIND == KIND_CONV ? 2 : 4;  // K=8 MMAs per sub-tile
     static constexpr int KS = KIND == KIND_CONV ? 16 * CG : 32;  // K elements per stage
+    static constexpr int NK = KS / 8;                                // K=8 MMA steps per stage
+    // B-descriptor advance (16-byte units) of K=8 step j within a stage
+    __host__ __device__ static constexpr uint32_t boff(int j) {
+        return KIND == KIND_GEMM ? (uint32_t)(j * 64)                   // 8 k-rows x 128 B
+             : KIND == KIND_CONV ? (uint32_t)(((j * 32) / B_ROW * B_SUB + (j * 32) % B_ROW) / 16)
+                                 : (uint32_t)(j * 2 * BN);             // stem: 2 taps x BN x 16 B
+    }
 };
 
 constexpr int kStemMaxR = 7;  // resident stem weights: R <= 7 kernel rows
@@ -335,10 +372,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             int s = 0;
             uint32_t ph = 0;
+            int kglob = 0;
             for (int st = cid; st < num_super; st += ncl) {
                 const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
                     mbar_wait(&empty[s], ph ^ 1);
+                    trace_ev(p, TR_P_ISSUE, kglob);
                     uint8_t *sp = smem + s * L::STAGE;
                     mbar_arrive_expect_tx(&full[s], tx);
                     if (KIND == KIND_GEMM) {
@@ -394,8 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer (one thread) =====================
-        if (lane == 0) {
+        // ===================== MMA issuer (whole warp, one elected lane issues) ============
+        {
             constexpr uint32_t idesc = idesc_tf32(128, BN, KIND == KIND_GEMM ? 1 : 0);
             if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
                 mbar_wait(wfull, 0);
@@ -403,71 +442,87 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             int s = 0, t = 0;
             uint32_t ph = 0, tph = 0;
-            int g = 0;
+            int g = 0, kglob = 0;
+            const int num_kb = p.num_kb;
             for (int st_i = cid; st_i < num_super; st_i += ncl) {
                 int in_seg = 0;
                 uint32_t d_tmem = tmem_base;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = 0; kb < num_kb; ++kb, ++kglob) {
                     if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
                         mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
                         tc_fence_after();
                         d_tmem = tmem_base + (uint32_t)((g & 1) * BN);
                     }
+                    if (lane == 0) trace_ev(p, TR_M_LOOP, kglob);
                     if (TS) mbar_wait(&tready[t], tph);
                     else mbar_wait(&full[s], ph);
+                    if (lane == 0) trace_ev(p, TR_M_WAITED, kglob);
                     tc_fence_after();
+                    if (lane == 0) trace_ev(p, TR_M_READY, kglob);
                     const uint32_t st = smem0 + s * L::STAGE;
                     const uint32_t a_t = tmem_base + L::A_SLOT0 + t * L::SLOT_COLS;
+                    if constexpr (TS) {
+                        // k-block base descriptors (step offsets are immediates in the asm)
+                        uint64_t bhi, blo;
+                        if (KIND == KIND_GEMM) {
+                            // MN-major tf32 operand: 128B rows of 32 n-values, 32B-atom swizzle
+                            // (SWIZZLE_128B_BASE32B); 4-row k-groups at SBO = 512B, 32-col
+                            // chunks at LBO = 32 rows * 128B.
+                            bhi = smem_desc(st + L::B_HI, 4096, 512, LAYOUT_SW128_B32);
+                            blo = smem_desc(st + L::B_LO, 4096, 512, LAYOUT_SW128_B32);
+                        } else if (KIND == KIND_CONV) {
+                            const uint32_t lay = G::B_ROW == 128 ? LAYOUT_SW128 : LAYOUT_SW64;
+                            bhi = smem_desc(st + L::B_HI, 16, 8 * G::B_ROW, lay);
+                            blo = smem_desc(st + L::B_LO, 16, 8 * G::B_ROW, lay);
+                        } else {
+                            // resident no-swizzle K-major weights: 8-row x 16B core matrices;
+                            // taps (2j, 2j+1) are BN*16 B apart
+                            const uint32_t w = smem0 + L::W_OFF + (uint32_t)(kb * 8 * BN * 16);
+                            bhi = smem_desc(w, BN * 16, 128, 0);
+                            blo = smem_desc(w + kStemMaxR * 8 * BN * 16, BN * 16, 128, 0);
+                        }
+                        mma_ts_block<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
+                                     G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
+                            d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < G::NSUB; ++c) {
+                        for (int c = 0; c < G::NSUB; ++c) {
 #pragma unroll
-                        for (int kk = 0; kk < G::KK; ++kk) {
-                            uint64_t bhi, blo;
-                            if (KIND == KIND_GEMM) {
-                                // MN-major tf32 operand: 128B rows of 32 n-values, 32B-atom
-                                // swizzle (SWIZZLE_128B_BASE32B); 4-row k-groups at SBO = 512B,
-                                // 32-col chunks at LBO = 32 rows * 128B.
-                                bhi = smem_desc(st + L::B_HI + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
-                                blo = smem_desc(st + L::B_LO + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
-                            } else if (KIND == KIND_CONV) {
-                                const uint32_t kbyte = (c * G::KK + kk) * 32;  // K=8 step -> 32 B
-                                const uint32_t b_off = (kbyte / G::B_ROW) * G::B_SUB + kbyte % G::B_ROW;
-                                const uint32_t lay = G::B_ROW == 128 ? LAYOUT_SW128 : LAYOUT_SW64;
-                                bhi = smem_desc(st + L::B_HI + b_off, 16, 8 * G::B_ROW, lay);
-                                blo = smem_desc(st + L::B_LO + b_off, 16, 8 * G::B_ROW, lay);
-                            } else {
-                                // resident no-swizzle K-major weights: 8-row x 16B core
-                                // matrices; taps (2kk, 2kk+1) are BN*16 B apart
-                                const uint32_t w = smem0 + L::W_OFF + (uint32_t)((kb * 8 + kk * 2) * BN * 16);
-                                bhi = smem_desc(w, BN * 16, 128, 0);
-                                blo = smem_desc(w + kStemMaxR * 8 * BN * 16, BN * 16, 128, 0);
-                            }
-                            const uint32_t acc = (in_seg | c | kk) != 0;
-                            if (TS) {
-                                const uint32_t ahi = a_t + c * 16 + kk * 8;
-                                mma_tf32_ts(d_tmem, ahi, bhi, idesc, acc);
-                                if (SPLIT3) {
-                                    mma_tf32_ts(d_tmem, ahi, blo, idesc, 1);
-                                    mma_tf32_ts(d_tmem, ahi + G::KS, bhi, idesc, 1);
+                            for (int kk = 0; kk < G::KK; ++kk) {
+                                uint64_t bhi;
+                                if (KIND == KIND_GEMM) {
+                                    bhi = smem_desc(st + L::B_HI + kk * 1024, 4096, 512, LAYOUT_SW128_B32);
+                                } else {
+                                    const uint32_t kbyte = (c * G::KK + kk) * 32;  // K=8 step -> 32 B
+                                    const uint32_t b_off = (kbyte / G::B_ROW) * G::B_SUB + kbyte % G::B_ROW;
+                                    const uint32_t lay = G::B_ROW == 128 ? LAYOUT_SW128 : LAYOUT_SW64;
+                                    bhi = smem_desc(st + L::B_HI + b_off, 16, 8 * G::B_ROW, lay);
                                 }
-                            } else {
+                                const uint32_t acc = (in_seg | c | kk) != 0;
                                 const uint32_t layout = KIND == KIND_GEMM ? LAYOUT_SW128 : LAYOUT_SW64;
                                 const uint32_t a_sbo = KIND == KIND_GEMM ? 1024 : 512;
                                 const uint32_t a_off = c * G::A_SUB + kk * 32;
                                 const uint64_t ahi = smem_desc(st + L::A_OFF + a_off, 16, a_sbo, layout);
-                                mma_tf32(d_tmem, ahi, bhi, idesc, acc);
+                                mma1_ss_elect(d_tmem, ahi, bhi, idesc, acc);
                             }
                         }
                     }
-                    if (KIND != KIND_STEM) {  // B (and SS-mode A) consumed, in every CTA
-                        if (CL == 1) mma_commit(&empty[s]);
-                        else mma_commit_mc(&empty[s], cl_mask);
+                    // release the stage (B, and SS-mode A; in every CTA of the cluster)
+                    // and the TMEM A slot
+                    if (KIND != KIND_STEM && TS && CL == 1) {
+                        mma_commit2_elect(&empty[s], &tfree[t]);
+                    } else {
+                        if (KIND != KIND_STEM) {
+                            if (CL == 1) mma_commit_elect(&empty[s]);
+                            else mma_commit_mc_elect(&empty[s], cl_mask);
+                        }
+                        if (TS) mma_commit_elect(&tfree[t]);
                     }
-                    if (TS) mma_commit(&tfree[t]);                 // A slot consumed
+                    if (lane == 0) trace_ev(p, TR_M_ISSUED, kglob);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if (++t == TSLOTS) { t = 0; tph ^= 1; }
-                    if (++in_seg == seg_kb || kb + 1 == p.num_kb) {
-                        mma_commit(&tmem_full[g & 1]);
+                    if (++in_seg == seg_kb || kb + 1 == num_kb) {
+                        mma_commit_elect(&tmem_full[g & 1]);
                         in_seg = 0;
                         ++g;
                     }
@@ -483,9 +538,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
             int s = 0, t = 0;
             uint32_t ph = 0, tph = 0;
+            int kglob = 0;
+            const bool tr = tid == 0;
             for (int st_i = cid; st_i < num_super; st_i += ncl) {
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
                     mbar_wait(&full[s], ph);
+                    if (tr) trace_ev(p, TR_S_FULL, kglob);
                     const uint32_t sa = smem0 + s * L::STAGE + L::A_OFF;
                     const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + t * L::SLOT_COLS;
                     if (KIND == KIND_GEMM) {
@@ -518,6 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         mbar_arrive(&empty[s]);  // A rows read
                         mbar_wait(&tfree[t], tph ^ 1);
+                        if (tr) trace_ev(p, TR_S_TFREE, kglob);
                         tc_fence_after();
                         if (!(p.flags & DBG_NO_STAGE_ST)) {
                             // fully unrolled: x[] must stay in registers and the warp-collective
@@ -557,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_wait_st();
                     tc_fence_before();
                     mbar_arrive(&tready[t]);
+                    if (tr) trace_ev(p, TR_S_DONE, kglob);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if (++t == TSLOTS) { t = 0; tph ^= 1; }
                 }
@@ -570,13 +630,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
-        int g = 0;
-        for (int st_i = cid; st_i < num_super; st_i += ncl) {
+        const bool tr = e == 0 && lane == 0;
+        int g = 0, jt = 0;
+        for (int st_i = cid; st_i < num_super; st_i += ncl, ++jt) {
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
             float sum[HALF];
             for (int sg = 0; sg < nseg; ++sg, ++g) {
                 mbar_wait(&tmem_full[g & 1], (g >> 1) & 1);
                 tc_fence_after();
+                if (tr) trace_ev(p, TR_E_FULL, g);
                 const uint32_t base = tmem_base + lane_off + (uint32_t)((g & 1) * BN + half * HALF);
                 if (sg == 0) {
                     // first segment: load straight into the sums (all loads in flight, one wait)
@@ -596,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tc_fence_before();
                 mbar_arrive(&tmem_empty[g & 1]);
+                if (tr) trace_ev(p, TR_E_DRAINED, g);
             }
             // ---- store (bias + ReLU fused) ----
             bool valid;
@@ -629,6 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (tr) trace_ev(p, TR_E_STORED, jt);
         }
     }
     __syncwarp();

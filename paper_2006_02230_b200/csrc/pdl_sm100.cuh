@@ -160,6 +160,153 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-converged issue: the whole warp executes these, elect.sync picks one lane
+// (always the same, the lowest) to issue.  Issuing from divergent lane-0 code
+// makes the compiler wrap every tcgen05 instruction in an elect/branch loop
+// (~70 cycles per MMA measured) -- slower than the MMA itself at N <= 128.
+// 3xTF32 step: D += Ahi*Bhi (or = when acc == 0), D += Ahi*Blo, D += Alo*Bhi.
+__device__ __forceinline__ void mma3_ts_elect(uint32_t d, uint32_t a_hi, uint32_t a_lo,
+                                              uint64_t bhi, uint64_t blo, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "setp.eq.b32 t, %6, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, t;\n\t"
+        "}" ::"r"(d),
+        "r"(a_hi), "r"(a_lo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma1_ts_elect(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n\t"
+        "}" ::"r"(d),
+        "r"(a), "l"(b), "r"(acc), "r"(idesc)
+        : "memory");
+}
+__device__ __forceinline__ void mma1_ss_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t"
+        "}" ::"r"(d),
+        "l"(a), "l"(b), "r"(acc), "r"(idesc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+        "}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc_elect(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+// A whole k-block of TS-form MMAs from ONE asm statement: NK K=8 steps, each
+// D += Ahi*Bhi (+ Ahi*Blo + Alo*Bhi for 3xTF32).  A step j reads TMEM columns
+// a + 8j (hi) and a + KS + 8j (lo); B descriptors are bhi/blo advanced by the
+// compile-time 16-byte offset BOFF(j).  One elect.sync for the block keeps the
+// issue stream to ~5 instructions per MMA (no per-MMA R2UR / vote / branch).
+#define PDL_TS_STEP(J, OFF, SPLIT, FIRSTPRED)                                          \
+    "add.u32 ah, %1, " #J "*8;\n\t"                                                     \
+    "add.u64 bh, %2, " OFF ";\n\t"                                                      \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %4, " FIRSTPRED ";\n\t"     \
+    SPLIT
+#define PDL_TS_LO(OFF)                                                                 \
+    "add.u32 al, ah, %6;\n\t"                                                           \
+    "add.u64 bl, %3, " OFF ";\n\t"                                                      \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %4, t;\n\t"                 \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %4, t;\n\t"
+
+template <int NK, bool SPLIT3, uint32_t KS, uint32_t O0, uint32_t O1, uint32_t O2, uint32_t O3,
+          uint32_t O4 = 0, uint32_t O5 = 0, uint32_t O6 = 0, uint32_t O7 = 0>
+__device__ __forceinline__ void mma_ts_block(uint32_t d, uint32_t a, uint64_t bhi, uint64_t blo,
+                                             uint32_t idesc, uint32_t acc) {
+    static_assert(NK == 2 || NK == 4 || NK == 8, "k-steps per block");
+#define PDL_LO(OFF) (SPLIT3 ? PDL_TS_LO(OFF) : "")
+    if constexpr (NK == 2) {
+        if constexpr (SPLIT3)
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP(0, "%7", PDL_TS_LO("%7"), "p") PDL_TS_STEP(1, "%8", PDL_TS_LO("%8"), "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP(0, "%7", "", "p") PDL_TS_STEP(1, "%8", "", "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1) : "memory");
+    } else if constexpr (NK == 4) {
+        if constexpr (SPLIT3)
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP(0, "%7", PDL_TS_LO("%7"), "p") PDL_TS_STEP(1, "%8", PDL_TS_LO("%8"), "t")
+                         PDL_TS_STEP(2, "%9", PDL_TS_LO("%9"), "t") PDL_TS_STEP(3, "%10", PDL_TS_LO("%10"), "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP(0, "%7", "", "p") PDL_TS_STEP(1, "%8", "", "t")
+                         PDL_TS_STEP(2, "%9", "", "t") PDL_TS_STEP(3, "%10", "", "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3) : "memory");
+    } else {
+        if constexpr (SPLIT3)
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP(0, "%7", PDL_TS_LO("%7"), "p") PDL_TS_STEP(1, "%8", PDL_TS_LO("%8"), "t")
+                         PDL_TS_STEP(2, "%9", PDL_TS_LO("%9"), "t") PDL_TS_STEP(3, "%10", PDL_TS_LO("%10"), "t")
+                         PDL_TS_STEP(4, "%11", PDL_TS_LO("%11"), "t") PDL_TS_STEP(5, "%12", PDL_TS_LO("%12"), "t")
+                         PDL_TS_STEP(6, "%13", PDL_TS_LO("%13"), "t") PDL_TS_STEP(7, "%14", PDL_TS_LO("%14"), "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3), "n"(O4), "n"(O5), "n"(O6), "n"(O7)
+                         : "memory");
+        else
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP(0, "%7", "", "p") PDL_TS_STEP(1, "%8", "", "t")
+                         PDL_TS_STEP(2, "%9", "", "t") PDL_TS_STEP(3, "%10", "", "t")
+                         PDL_TS_STEP(4, "%11", "", "t") PDL_TS_STEP(5, "%12", "", "t")
+                         PDL_TS_STEP(6, "%13", "", "t") PDL_TS_STEP(7, "%14", "", "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3), "n"(O4), "n"(O5), "n"(O6), "n"(O7)
+                         : "memory");
+    }
+#undef PDL_LO
+}
+
+// Two commits (stage release, A-slot release) from one elected lane.
+__device__ __forceinline__ void mma_commit2_elect(uint64_t *bar0, uint64_t *bar1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t"
+        "}" ::"r"(smem_u32(bar0)), "r"(smem_u32(bar1))
+        : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile(
