@@ -10,4 +10,9 @@ from ._lib import PdlDeviceError, PdlError, PdlShapeError, TileCfg  # noqa: F401
 from .ops import (PackedWeights, bias_relu_, conv2d_nchw16c, conv_out_hw,  # noqa: F401
                   device_ok, gemm, prepack_weights)
 
+from .loopnest import (LoopDslError, LoopNest, NonAffineError, ParseError, Program,  # noqa: F401
+                       parse, parse_program, pretty, reinstate_microkernel,
+                       substitute_microkernel)
+from .executor import InterpreterError, execute, interpret, make_inputs, plan_program  # noqa: F401
+
 __version__ = "0.1.0"
