@@ -1,0 +1,425 @@
+"""Ranking tile-engine variants: Eq. 1 cost, the pairwise DNN judge, and a
+B200 pipeline model.
+
+API mirror of `looprank.rank` (/root/reference/pkg/src/looprank/rank.py):
+  VariantStats (:36-55)       per-level working-set bytes; on the B200 the
+                              three levels are SMEM, TMEM, L2 (machines/b200.json)
+  cost / cost_of_stats (:76-98)   Eq. 1, exact rationals (fractions.Fraction)
+  rank_by_cost (:101-113)     ascending cost, ties by variant id
+  pair_features (:117-128)    8 jointly normalised statistics
+  RankerModel (:144-194)      8-64-32-16-8-2 MLP, relu/relu/softsign/relu,
+                              softmax output; .npz files with the same keys
+  dnn_judge (:197-206)        win1 / win2 / draw at threshold theta
+  tournament_rank (:209-237)  all unordered pairs, rank by wins then id
+  TrainConfig / train_ranker / loss_and_gradients (:241-338)
+  save_dataset / load_dataset (:341-364)   same CSV header
+so reference-produced datasets and models load unchanged.
+
+B200 additions: `stats_for_variant` (tile working sets -> Alg. 2 -> stats),
+`PipelineModel` / `predict_seconds` (the tile engine's cost: per-k-block
+tensor-pipe time vs operand feed, wave quantisation, HBM floor, with constants
+fitted on measured B200 sweeps) and `rank_by_model`.
+"""
+from __future__ import annotations
+
+import csv
+import json
+import math
+import os
+import warnings
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Sequence
+
+import numpy as np
+
+LAYER_DIMS = (8, 64, 32, 16, 8, 2)
+ACTIVATIONS = ("relu", "relu", "softsign", "relu")
+DEFAULT_THETA = 0.6
+_CSV_HEADER = ["a_l1", "a_l2", "a_l3", "a_mem", "b_l1", "b_l2", "b_l3", "b_mem", "label"]
+
+
+class RankError(Exception):
+    pass
+
+
+@dataclass(frozen=True)
+class VariantStats:
+    """Working-set bytes placed at each level (l1 = SMEM, l2 = TMEM, l3 = L2 on
+    the B200 machine file) plus the bytes left to memory."""
+    variant_id: str
+    ws_l1: float
+    ws_l2: float
+    ws_l3: float
+    ws_mem: float
+
+    @classmethod
+    def from_assignment(cls, variant_id: str, a) -> "VariantStats":
+        per_level = [b for _, b in a.level_bytes]
+        if len(per_level) > 3:
+            raise RankError("statistics carry at most three levels")
+        per_level = (per_level + [0, 0, 0])[:3]
+        return cls(variant_id, *(float(b) for b in per_level), float(a.mem_bytes))
+
+    def vector(self) -> np.ndarray:
+        return np.asarray((self.ws_l1, self.ws_l2, self.ws_l3, self.ws_mem), dtype=np.float64)
+
+
+@dataclass(frozen=True)
+class RankedList:
+    method: str
+    order: tuple
+    scores: tuple
+
+    def top(self, k: int) -> tuple:
+        return self.order[:max(k, 1)]
+
+    def to_dict(self) -> dict:
+        return {"method": self.method, "order": list(self.order), "scores": dict(self.scores)}
+
+
+# ----------------------------------------------------------------------------- Eq. 1
+def _weighted(levels, sizes, m) -> Fraction:
+    acc = Fraction(0)
+    for lv, nbytes in zip(levels, sizes):
+        if lv.bandwidth == 0:
+            raise RankError(f"level {lv.name} has zero bandwidth")
+        acc += Fraction(nbytes) * Fraction(lv.latency) / Fraction(lv.bandwidth)
+    if m.mem_bandwidth == 0:
+        raise RankError("memory has zero bandwidth")
+    return acc
+
+
+def cost(assignment, m) -> Fraction:
+    """C = sum_i WS_i * lat_i / bw_i + WS_mem * lat_mem / bw_mem (Eq. 1)."""
+    c = _weighted(m.levels, [assignment.level_total(lv.name) for lv in m.levels], m)
+    return c + Fraction(assignment.mem_bytes) * Fraction(m.mem_latency) / Fraction(m.mem_bandwidth)
+
+
+def cost_of_stats(stats: VariantStats, m) -> Fraction:
+    sizes = (stats.ws_l1, stats.ws_l2, stats.ws_l3)[:len(m.levels)]
+    c = _weighted(m.levels[:len(sizes)], sizes, m)
+    return c + Fraction(stats.ws_mem) * Fraction(m.mem_latency) / Fraction(m.mem_bandwidth)
+
+
+def rank_by_cost(stats: Sequence[VariantStats], m) -> RankedList:
+    if not stats:
+        raise RankError("no variants to rank")
+    scored = sorted((cost_of_stats(s, m), s.variant_id) for s in stats)
+    return RankedList("cost", tuple(v for _, v in scored), tuple((v, float(c)) for c, v in scored))
+
+
+# ----------------------------------------------------------------------------- DNN judge
+def pair_features(v1: VariantStats, v2: VariantStats) -> np.ndarray:
+    """Both variants' statistics divided by their joint sum (joint, not per
+    variant: the judge needs the relative magnitudes across the pair)."""
+    raw = np.concatenate((v1.vector(), v2.vector()))
+    s = float(raw.sum())
+    if s == 0.0:
+        warnings.warn("pair of all-zero statistics; returning the uniform vector")
+        return np.full(8, 0.125)
+    return raw / s
+
+
+def _relu(z):
+    return np.maximum(z, 0.0)
+
+
+def _softsign(z):
+    return z / (1.0 + np.abs(z))
+
+
+_ACT = {"relu": (_relu, lambda z: (z > 0).astype(z.dtype)),
+        "softsign": (_softsign, lambda z: 1.0 / np.square(1.0 + np.abs(z)))}
+
+
+def _softmax(z):
+    z = z - z.max(axis=1, keepdims=True)
+    e = np.exp(z)
+    return e / e.sum(axis=1, keepdims=True)
+
+
+@dataclass
+class RankerModel:
+    weights: list
+    biases: list
+    theta: float = DEFAULT_THETA
+
+    @classmethod
+    def initialize(cls, seed: int = 0, theta: float = DEFAULT_THETA) -> "RankerModel":
+        """U(-1/sqrt(fan_in), 1/sqrt(fan_in)) weights, zero biases, seeded."""
+        rng = np.random.default_rng(seed)
+        ws, bs = [], []
+        for fi, fo in zip(LAYER_DIMS[:-1], LAYER_DIMS[1:]):
+            lim = 1.0 / math.sqrt(fi)
+            ws.append(rng.uniform(-lim, lim, size=(fo, fi)))
+            bs.append(np.zeros(fo))
+        return cls(ws, bs, theta)
+
+    def _layers(self, X):
+        """Pre-activations and activations of every layer (for backprop)."""
+        pre, post = [], [X]
+        h = X
+        last = len(self.weights) - 1
+        for i, (w, b) in enumerate(zip(self.weights, self.biases)):
+            z = h @ w.T + b
+            pre.append(z)
+            h = z if i == last else _ACT[ACTIVATIONS[i]][0](z)
+            post.append(h)
+        return pre, post
+
+    def forward_batch(self, X: np.ndarray) -> np.ndarray:
+        _, post = self._layers(np.atleast_2d(X))
+        p = _softmax(post[-1])
+        if not np.isfinite(p).all():
+            raise RankError("non-finite network output (corrupted weights?)")
+        return p
+
+    def forward(self, x: np.ndarray) -> np.ndarray:
+        return self.forward_batch(np.asarray(x)[None])[0]
+
+    def save(self, path: str) -> None:
+        blob = {"version": np.array([1]), "theta": np.array([self.theta]),
+                "dims": np.array(LAYER_DIMS)}
+        for i, w in enumerate(self.weights):
+            blob[f"w{i}"] = w
+            blob[f"b{i}"] = self.biases[i]
+        np.savez(path, **blob)
+
+    @classmethod
+    def load(cls, path: str) -> "RankerModel":
+        with np.load(path) as f:
+            if int(f["version"][0]) != 1:
+                raise RankError("unknown ranker file version")
+            if tuple(int(d) for d in f["dims"]) != LAYER_DIMS:
+                raise RankError("ranker file has other layer dimensions")
+            n = len(LAYER_DIMS) - 1
+            return cls([f[f"w{i}"] for i in range(n)], [f[f"b{i}"] for i in range(n)],
+                       float(f["theta"][0]))
+
+
+def dnn_judge(model: RankerModel, v1: VariantStats, v2: VariantStats) -> str:
+    """"win1" / "win2" when that side's probability exceeds theta (> 0.5, so at
+    most one side can), else "draw"."""
+    p = model.forward(pair_features(v1, v2))
+    return "win1" if p[0] > model.theta else "win2" if p[1] > model.theta else "draw"
+
+
+def tournament_rank(model: RankerModel, stats: Sequence[VariantStats],
+                    both_directions: bool = False) -> RankedList:
+    if len(stats) < 2:
+        raise RankError("a tournament needs two or more variants")
+    entrants = sorted(stats, key=lambda s: s.variant_id)
+    wins = dict.fromkeys((s.variant_id for s in entrants), 0)
+
+    def play(a, b):
+        r = dnn_judge(model, a, b)
+        if r != "draw":
+            wins[(a if r == "win1" else b).variant_id] += 1
+
+    for i, a in enumerate(entrants):
+        for b in entrants[i + 1:]:
+            play(a, b)
+            if both_directions:
+                play(b, a)
+    order = sorted(wins, key=lambda v: (-wins[v], v))
+    return RankedList("dnn", tuple(order), tuple((v, float(wins[v])) for v in order))
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    learning_rate: float = 0.1
+    epochs: int = 300
+    batch_size: int = 32
+    seed: int = 0
+    val_fraction: float = 0.3
+    theta: float = DEFAULT_THETA
+
+
+@dataclass
+class TrainResult:
+    model: RankerModel
+    train_accuracy: float
+    val_accuracy: float
+    final_loss: float
+    epochs_run: int
+
+
+def loss_and_gradients(model: RankerModel, X: np.ndarray, y: np.ndarray):
+    """Mean softmax cross-entropy and its gradients w.r.t. every weight/bias."""
+    pre, post = model._layers(X)
+    p = _softmax(post[-1])
+    n = len(X)
+    rows = np.arange(n)
+    loss = float(-np.mean(np.log(p[rows, y] + 1e-12)))
+    g = p.copy()
+    g[rows, y] -= 1.0
+    g /= n
+    gw, gb = [None] * len(model.weights), [None] * len(model.weights)
+    for i in range(len(model.weights) - 1, -1, -1):
+        gw[i] = g.T @ post[i]
+        gb[i] = g.sum(axis=0)
+        if i:
+            g = (g @ model.weights[i]) * _ACT[ACTIVATIONS[i - 1]][1](pre[i - 1])
+    return loss, gw, gb, p
+
+
+def _accuracy(model, X, y) -> float:
+    if not len(X):
+        return float("nan")
+    return float(np.mean(model.forward_batch(X).argmax(axis=1) == y))
+
+
+def train_ranker(dataset, config: TrainConfig = TrainConfig()) -> TrainResult:
+    """Seeded mini-batch SGD; label 0 = first variant faster, 1 = second."""
+    if not dataset:
+        raise RankError("empty training dataset")
+    X = np.stack([pair_features(a, b) for a, b, _ in dataset])
+    y = np.asarray([lab for _, _, lab in dataset], dtype=np.int64)
+    if set(np.unique(y).tolist()) - {0, 1}:
+        raise RankError("labels must be 0 or 1")
+    rng = np.random.default_rng(config.seed)
+    shuffle = rng.permutation(len(X))
+    X, y = X[shuffle], y[shuffle]
+    nv = int(len(X) * config.val_fraction)
+    Xv, yv, Xt, yt = X[:nv], y[:nv], X[nv:], y[nv:]
+    if not len(Xt):
+        Xt, yt = X, y
+    model = RankerModel.initialize(config.seed, config.theta)
+    loss = float("nan")
+    for _ in range(config.epochs):
+        perm = rng.permutation(len(Xt))
+        for s in range(0, len(Xt), config.batch_size):
+            b = perm[s:s + config.batch_size]
+            loss, gw, gb, _ = loss_and_gradients(model, Xt[b], yt[b])
+            if not math.isfinite(loss):
+                raise RankError(f"training diverged (loss {loss})")
+            for i in range(len(model.weights)):
+                model.weights[i] -= config.learning_rate * gw[i]
+                model.biases[i] -= config.learning_rate * gb[i]
+    return TrainResult(model, _accuracy(model, Xt, yt), _accuracy(model, Xv, yv), loss,
+                       config.epochs)
+
+
+def save_dataset(path: str, rows) -> None:
+    with open(path, "w", newline="") as fh:
+        out = csv.writer(fh)
+        out.writerow(_CSV_HEADER)
+        for a, b, lab in rows:
+            out.writerow([*a.vector().tolist(), *b.vector().tolist(), int(lab)])
+
+
+def load_dataset(path: str) -> list:
+    rows = []
+    with open(path, newline="") as fh:
+        rd = csv.reader(fh)
+        if next(rd) != _CSV_HEADER:
+            raise RankError("dataset header does not match")
+        for k, r in enumerate(rd):
+            v = [float(t) for t in r[:8]]
+            rows.append((VariantStats(f"a{k}", *v[:4]), VariantStats(f"b{k}", *v[4:]), int(r[8])))
+    return rows
+
+
+# ----------------------------------------------------------------------------- B200 side
+def stats_for_variant(layer, variant, n_images: int, machine=None) -> VariantStats:
+    """Tile working sets -> Alg. 2 placement on the per-SM B200 machine -> stats."""
+    from .machine import assign_to_caches, default_machine, effective_sizes
+    from .wset import tile_working_sets
+    m = machine or default_machine()
+    m = effective_sizes(m, m.cores)
+    rep = tile_working_sets(layer, variant, n_images, sms=m.cores)
+    return VariantStats.from_assignment(variant.vid, assign_to_caches(rep, m))
+
+
+_MODEL_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "machines",
+                           "b200_engine.json")
+
+
+@dataclass
+class PipelineModel:
+    """Per-tile cost of the persistent tile engine, in SM cycles.
+
+    k-block time = max(tensor pipe, operand feed, fixed handshake):
+      pipe  = mmas_per_kblock * (mma_fixed + mma_per_n * BN)
+      feed  = bytes_per_kblock / l2_bytes_per_cycle   (cluster multicast divides B)
+      fixed = kblock_fixed
+    tile time = num_kb * k-block time + tile_fixed;  waves over the resident
+    CTAs; floor at the compulsory HBM bytes.  Constants are fitted on measured
+    B200 sweeps (scripts/sweep_variants.py -> machines/b200_engine.json)."""
+    mma_fixed: float = 10.0
+    mma_per_n: float = 0.6
+    l2_bytes_per_cycle: float = 64.0
+    kblock_fixed: float = 120.0
+    tile_fixed: float = 900.0
+    launch_us: float = 4.0
+    clock_ghz: float = 1.92
+    hbm_gbs: float = 6546.6
+    sms: int = 148
+    fitted_on: str = "defaults"
+
+    @classmethod
+    def load(cls, path: str = _MODEL_FILE) -> "PipelineModel":
+        if not os.path.exists(path):
+            return cls()
+        with open(path) as fh:
+            d = json.load(fh)
+        return cls(**{k: v for k, v in d.items() if k in cls.__dataclass_fields__})
+
+    def save(self, path: str = _MODEL_FILE) -> None:
+        with open(path, "w") as fh:
+            json.dump({k: getattr(self, k) for k in self.__dataclass_fields__}, fh, indent=1)
+
+    def terms(self, layer, variant, n_images: int) -> dict:
+        from .variants import engine_geometry
+        g = engine_geometry(layer, variant, n_images, self.sms)
+        split = variant.mode == "3xtf32"
+        mmas = (3 if split else 1) * (g["ks"] // 8)
+        planes = 2 if split else 1
+        a_bytes = 128 * g["ks"] * 4
+        b_bytes = variant.bn * g["ks"] * 4 * planes / variant.cluster
+        ctas = (self.sms // variant.cluster) * variant.cluster
+        waves = math.ceil(g["tiles"] / ctas)
+        return {"num_kb": g["num_kb"], "mmas": mmas, "feed_bytes": a_bytes + b_bytes,
+                "waves": waves, "bn": variant.bn,
+                "hbm_bytes": layer.bytes(n_images) if hasattr(layer, "bytes") else 0}
+
+    def predict_cycles_per_tile(self, t: dict) -> float:
+        pipe = t["mmas"] * (self.mma_fixed + self.mma_per_n * t["bn"])
+        feed = t["feed_bytes"] / self.l2_bytes_per_cycle
+        kb = max(pipe, feed, self.kblock_fixed)
+        return t["num_kb"] * kb + self.tile_fixed
+
+    def predict_seconds(self, layer, variant, n_images: int) -> float:
+        t = self.terms(layer, variant, n_images)
+        compute = t["waves"] * self.predict_cycles_per_tile(t) / (self.clock_ghz * 1e9)
+        hbm = t["hbm_bytes"] / (self.hbm_gbs * 1e9)
+        return max(compute, hbm) + self.launch_us * 1e-6
+
+
+def predict_seconds(layer, variant, n_images: int, model: PipelineModel = None) -> float:
+    return (model or PipelineModel.load()).predict_seconds(layer, variant, n_images)
+
+
+def rank_by_model(layer, variants, n_images: int, model: PipelineModel = None) -> RankedList:
+    if not variants:
+        raise RankError("no variants to rank")
+    pm = model or PipelineModel.load()
+    scored = sorted((pm.predict_seconds(layer, v, n_images), v.vid) for v in variants)
+    return RankedList("model", tuple(v for _, v in scored), tuple((v, s) for s, v in scored))
+
+
+def kendall_tau(order_a: Sequence[str], order_b: Sequence[str]) -> float:
+    """Kendall rank correlation of two orderings of the same ids (tau-a)."""
+    ids = list(order_a)
+    if sorted(ids) != sorted(order_b):
+        raise RankError("orderings cover different ids")
+    n = len(ids)
+    if n < 2:
+        return 1.0
+    rb = {v: i for i, v in enumerate(order_b)}
+    s = 0
+    for i in range(n):
+        for j in range(i + 1, n):
+            s += 1 if rb[ids[i]] < rb[ids[j]] else -1
+    return s / (n * (n - 1) / 2)
