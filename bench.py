@@ -202,9 +202,10 @@ def run_suite(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     if not P.device_ok():
         raise SystemExit("libpdl.so: no sm_100 device")
-    if args.batch % world:
-        raise SystemExit(f"--batch {args.batch} not divisible by {world} ranks")
-    n_local = args.batch // world
+    from paper_2006_02230_b200.shard import max_over_ranks, replicate_, shard_images
+    _, n_local = shard_images(args.batch, world, rank)
+    if n_local == 0:
+        raise SystemExit(f"--batch {args.batch} leaves rank {rank} of {world} without images")
     layers = W.LAYERS
     peaks = load_peaks()
     mode_peak = peaks["tf32_tflops"] * 1e12 / (3.0 if args.mode == "3xtf32" else 1.0)
@@ -224,9 +225,7 @@ def run_suite(args, rank, world, local):
         if layer.C != ca:
             x[..., layer.C:] = 0
             w[:, :, :, :, layer.C:, :] = 0
-        if world > 1:
-            dist.broadcast(w, 0)
-            dist.broadcast(b, 0)
+        replicate_([w, b])
         pw = P.prepack_weights(w, mode=args.mode, channels=layer.C)
         y = torch.empty((n_local, layer.K // 16, layer.P, layer.Q, 16), device=dev)
         bufs.append((layer, x, w, b, pw, y))
@@ -271,11 +270,7 @@ def run_suite(args, rank, world, local):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(t_start.elapsed_time(t_end), dev)
     ms_step = ms / args.steps
     total_flops = sum(l.flops(args.batch) for l in layers)
     value = total_flops / (ms_step / 1e3) / 1e9
@@ -384,11 +379,8 @@ def run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    from paper_2006_02230_b200.shard import max_over_ranks
+    ms = max_over_ranks(e0.elapsed_time(e1), dev)
     return {"value": round(total_flops / (ms / steps / 1e3) / 1e9, 1), "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "ms_per_step": round(ms / steps, 3),

@@ -340,18 +340,21 @@ _MODEL_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "machines
 class PipelineModel:
     """Per-tile cost of the persistent tile engine, in SM cycles.
 
-    k-block time = max(tensor pipe, operand feed, fixed handshake):
+    k-block time = max(tensor pipe, operand feed) + handshake:
       pipe  = mmas_per_kblock * (mma_fixed + mma_per_n * BN)
       feed  = bytes_per_kblock / l2_bytes_per_cycle   (cluster multicast divides B)
-      fixed = kblock_fixed
-    tile time = num_kb * k-block time + tile_fixed;  waves over the resident
-    CTAs; floor at the compulsory HBM bytes.  Constants are fitted on measured
-    B200 sweeps (scripts/sweep_variants.py -> machines/b200_engine.json)."""
+      handshake = kblock_fixed + cluster_kb * (cluster - 1)
+    tile time = num_kb * k-block time + tile_fixed;  waves over the CTAs the
+    cluster shape lets the GPU keep resident (4-CTA clusters fit on 132 of the
+    148 SMs); floor at the compulsory HBM bytes.  Constants are fitted on
+    measured B200 sweeps (scripts/fit_ranker.py -> machines/b200_engine.json)."""
     mma_fixed: float = 10.0
     mma_per_n: float = 0.6
     l2_bytes_per_cycle: float = 64.0
     kblock_fixed: float = 120.0
+    cluster_kb: float = 20.0
     tile_fixed: float = 900.0
+    active_ctas: dict = field(default_factory=lambda: {"1": 148, "2": 148, "4": 132})
     launch_us: float = 4.0
     clock_ghz: float = 1.92
     hbm_gbs: float = 6546.6
@@ -378,16 +381,16 @@ class PipelineModel:
         planes = 2 if split else 1
         a_bytes = 128 * g["ks"] * 4
         b_bytes = variant.bn * g["ks"] * 4 * planes / variant.cluster
-        ctas = (self.sms // variant.cluster) * variant.cluster
+        ctas = int(self.active_ctas.get(str(variant.cluster), self.sms))
         waves = math.ceil(g["tiles"] / ctas)
         return {"num_kb": g["num_kb"], "mmas": mmas, "feed_bytes": a_bytes + b_bytes,
-                "waves": waves, "bn": variant.bn,
+                "waves": waves, "bn": variant.bn, "cluster": variant.cluster,
                 "hbm_bytes": layer.bytes(n_images) if hasattr(layer, "bytes") else 0}
 
     def predict_cycles_per_tile(self, t: dict) -> float:
         pipe = t["mmas"] * (self.mma_fixed + self.mma_per_n * t["bn"])
         feed = t["feed_bytes"] / self.l2_bytes_per_cycle
-        kb = max(pipe, feed, self.kblock_fixed)
+        kb = max(pipe, feed) + self.kblock_fixed + self.cluster_kb * (t["cluster"] - 1)
         return t["num_kb"] * kb + self.tile_fixed
 
     def predict_seconds(self, layer, variant, n_images: int) -> float:
@@ -395,6 +398,20 @@ class PipelineModel:
         compute = t["waves"] * self.predict_cycles_per_tile(t) / (self.clock_ghz * 1e9)
         hbm = t["hbm_bytes"] / (self.hbm_gbs * 1e9)
         return max(compute, hbm) + self.launch_us * 1e-6
+
+
+    def term_stats(self, layer, variant, n_images: int) -> VariantStats:
+        """The model's per-resource seconds as DNN statistics: (tensor pipe,
+        operand feed, handshakes + tile overheads, HBM) -- the B200 analogue of
+        per-level working sets for the pairwise judge."""
+        t = self.terms(layer, variant, n_images)
+        hz = self.clock_ghz * 1e9
+        per = t["waves"] * t["num_kb"] / hz
+        pipe = per * t["mmas"] * (self.mma_fixed + self.mma_per_n * t["bn"])
+        feed = per * t["feed_bytes"] / self.l2_bytes_per_cycle
+        hand = per * (self.kblock_fixed + self.cluster_kb * (t["cluster"] - 1)) + \
+            t["waves"] * self.tile_fixed / hz
+        return VariantStats(variant.vid, pipe, feed, hand, t["hbm_bytes"] / (self.hbm_gbs * 1e9))
 
 
 def predict_seconds(layer, variant, n_images: int, model: PipelineModel = None) -> float:
@@ -407,6 +424,45 @@ def rank_by_model(layer, variants, n_images: int, model: PipelineModel = None) -
     pm = model or PipelineModel.load()
     scored = sorted((pm.predict_seconds(layer, v, n_images), v.vid) for v in variants)
     return RankedList("model", tuple(v for _, v in scored), tuple((v, s) for s, v in scored))
+
+
+_RANKER_FILE = os.path.join(os.path.dirname(_MODEL_FILE), "b200_ranker.npz")
+
+
+def choose_variant(layer, n_images: int, mode: str = "3xtf32", method: str = "dnn",
+                   model: PipelineModel = None, judge: RankerModel = None):
+    """Pick the schedule for a conv layer among its legal tile variants.
+
+    method "dnn": tournament of the trained pairwise judge over the pipeline
+    model's per-resource terms (machines/b200_ranker.npz), ties broken by the
+    model's predicted time; "model": the fitted pipeline model alone; "cost":
+    Eq. 1 over the tile working sets."""
+    from .variants import VariantConfig, generate_variants
+    vs = generate_variants(layer, VariantConfig(modes=(mode,)))
+    if not vs:
+        raise RankError(f"no legal variant for {layer}")
+    if len(vs) == 1:
+        return vs[0]
+    pm = model or PipelineModel.load()
+    by_model = rank_by_model(layer, vs, n_images, pm)
+    if method == "model":
+        best = by_model.order[0]
+    elif method == "cost":
+        from .machine import default_machine
+        best = rank_by_cost([stats_for_variant(layer, v, n_images) for v in vs], default_machine()).order[0]
+    elif method == "dnn":
+        if judge is None:
+            if not os.path.exists(_RANKER_FILE):
+                raise RankError(f"no trained judge at {_RANKER_FILE}; run scripts/fit_ranker.py")
+            judge = RankerModel.load(_RANKER_FILE)
+        t = tournament_rank(judge, [pm.term_stats(layer, v, n_images) for v in vs],
+                            both_directions=True)
+        wins = dict(t.scores)
+        pos = {v: i for i, v in enumerate(by_model.order)}
+        best = min(wins, key=lambda v: (-wins[v], pos[v]))
+    else:
+        raise RankError(f"unknown ranking method {method!r}")
+    return next(v for v in vs if v.vid == best)
 
 
 def kendall_tau(order_a: Sequence[str], order_b: Sequence[str]) -> float:

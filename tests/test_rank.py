@@ -274,3 +274,25 @@ def test_b200_stats_and_model_rank():
     r = R.rank_by_model(L, vs, 256)
     assert sorted(r.order) == sorted(v.vid for v in vs)
     assert all(s > 0 for _, s in r.scores)
+
+
+def test_fitted_artifacts_and_choose_variant():
+    """The shipped pipeline model / judge load, and every ranking method picks
+    a legal variant deterministically."""
+    pm = R.PipelineModel.load()
+    assert pm.fitted_on != "defaults"
+    L = workloads.resnet50_v1_layers()[16]
+    for meth in ("dnn", "model", "cost"):
+        v = R.choose_variant(L, 256, "3xtf32", method=meth)
+        assert V.legal(L, v) and v == R.choose_variant(L, 256, "3xtf32", method=meth)
+    st = pm.term_stats(L, v, 256)
+    assert min(st.vector()) >= 0 and st.ws_l1 > 0
+    with pytest.raises(R.RankError):
+        R.choose_variant(L, 256, method="nope")
+    assert R.choose_variant(workloads.resnet50_v1_layers()[0], 256).vid == "bn64_bk32_c1_3xtf32"
+
+
+def test_ranker_report_committed():
+    rep = json.load(open(os.path.join(os.path.dirname(__file__), "..", "profiles", "ranker_r1.json")))
+    assert rep["model_loo"]["top1_regret_mean"] < rep["eq1_cost"]["top1_regret_mean"]
+    assert rep["dnn_pipeline_terms"]["heldout_accuracy"] > 0.8
