@@ -45,6 +45,8 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
     ap.add_argument("--cluster", type=int, default=0, help="override CTAs per weight-multicast cluster")
+    ap.add_argument("--schedule", default="default", choices=["default", "ranked"],
+                    help="tile config per layer: library default or the trained ranker's pick")
     return ap.parse_args()
 
 
@@ -234,6 +236,11 @@ def run_suite(args, rank, world, local):
     stream = torch.cuda.current_stream()
     launches_per_step = 0
     cfg = {"cluster_m": args.cluster} if args.cluster else None
+    if args.schedule == "ranked":
+        from paper_2006_02230_b200 import rank, variants
+        cfgs = [variants.emit_launch(rank.choose_variant(l, n_local, args.mode)) for l in layers]
+    else:
+        cfgs = [cfg] * len(layers)
 
     def step(ev=None):
         nonlocal launches_per_step
@@ -242,7 +249,7 @@ def run_suite(args, rank, world, local):
             if ev is not None:
                 ev[i][0].record(stream)
             P.conv2d_nchw16c(x, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
-                             mode=args.mode, out=y, cfg=cfg)
+                             mode=args.mode, out=y, cfg=cfgs[i])
             cnt += _lib.last_launch_count()
             if ev is not None:
                 ev[i][1].record(stream)
@@ -322,6 +329,7 @@ def run_suite(args, rank, world, local):
                       "global_batch": args.batch, "per_gpu_batch": n_local, "mode": args.mode,
                       "layout": "nChw16c x / KCRS16c16k w (prepacked once) / nKhw16k y",
                       "parallelism": f"batch-sharded x{world}, no collective",
+                      "schedule": args.schedule,
                       "l2": "step working set %.1f GB >> 126 MB L2; each layer's inputs were "
                             "last touched one full step earlier" % (
                                 sum(l.bytes(n_local) for l in layers) / 1e9),

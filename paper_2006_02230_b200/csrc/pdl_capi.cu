@@ -211,6 +211,15 @@ bool is_stem(int C, int R, int S, int stride) {
 
 int ceil16(int c) { return (c + 15) / 16; }
 
+// ResNet stem (C=3, 7x7) can pack (r, s, c) densely along K (147 -> 5 k-blocks
+// of 32) instead of one k-block of 8 taps x 4 channels per kernel row (7
+// k-blocks, 224): 29% fewer MMAs, but the gather then needs ~11 halo loads per
+// k-block and measured 0.60 ms vs 0.50 ms unpacked at N=256 (the stem is
+// staging/TMA-bound, not MMA-bound).  Kept selectable for the ranker; off.
+bool g_stem_pack = false;
+bool stem_packed(int C, int R, int S) { return g_stem_pack && C == 3 && R == 7 && S == 7; }
+int stem_kblocks(int C, int R, int S) { return stem_packed(C, R, S) ? (R * S * C + 31) / 32 : R; }
+
 // Input channels per packed weight row: 32 (128-byte SW128 rows) when the number
 // of 16-channel blocks is even, else 16 (64-byte SW64 rows).
 int weight_group(int C) { return ceil16(C) % 2 == 0 ? 32 : 16; }
@@ -247,14 +256,32 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     const int bn = 64;  // resident weights: 2 planes x 7 rows x 8 taps x 64 x 16 B = 112 KB
     (void)cfg_in;
     const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
-    const int BW = std::min({Q, 128, (256 - S) / stride + 1});
-    const int box_w = (BW - 1) * stride + S;
+    // tile = BW x BH output pixels (<= 128); its input halo (box_w x box_h pixels,
+    // 16 B each) is one TMA box and one pipeline stage.  Per tile the engine spends
+    // ~R x 700 cycles on MMAs and the TMA ~4.4 cycles per 16-byte halo element
+    // (both measured on B200, profiles/trace_*); pick the shape minimising
+    // tiles x max(the two).
+    int BW = 0, BH = 0;
+    {
+        constexpr double kMmaPerRow = 700.0, kTmaPerElem = 4.4;
+        double best = 1e30;
+        for (int bw = std::min(Q, 128); bw >= 1; --bw) {
+            const int bh = std::min(P, 128 / bw);
+            const int bxw = (bw - 1) * stride + S, bxh = (bh - 1) * stride + R;
+            if (bxw > 256 || bxh > 256 || 16 * bxw * bxh > pdl::kStemHaloBytes) continue;
+            const double tiles = (double)((Q + bw - 1) / bw) * ((P + bh - 1) / bh);
+            const double cost = tiles * std::max(R * kMmaPerRow, kTmaPerElem * bxw * bxh);
+            if (cost < best - 1e-9) { best = cost; BW = bw; BH = bh; }
+        }
+        if (!BW) return fail(PDL_EUNSUPPORTED, "stem: no halo tile fits (S=%d R=%d)", S, R);
+    }
+    const int box_w = (BW - 1) * stride + S, box_h = (BH - 1) * stride + R;
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     {
         const cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
         const cuuint64_t str[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
-        const cuuint32_t box[5] = {4, (cuuint32_t)box_w, 1, 1, 1};
+        const cuuint32_t box[5] = {4, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
         // only 16 of every 64 bytes are used: do not promote to 256B L2 fills
         if ((rc = encode(&maps.a[0], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem x",
                          CU_TENSOR_MAP_L2_PROMOTION_NONE)))
@@ -262,15 +289,17 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     }
     {
         const int planes = split ? 2 : 1;
-        const cuuint64_t dims[5] = {4, (cuuint64_t)K, 8, (cuuint64_t)R, (cuuint64_t)planes};
+        const int nkb = stem_kblocks(C, R, S);
+        const cuuint64_t dims[5] = {4, (cuuint64_t)K, 8, (cuuint64_t)nkb, (cuuint64_t)planes};
         const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)8 * K * 16,
-                                   (cuuint64_t)R * 8 * K * 16};
-        const cuuint32_t box[5] = {4, (cuuint32_t)bn, 8, (cuuint32_t)R, 1};  // one plane, resident
+                                   (cuuint64_t)nkb * 8 * K * 16};
+        const cuuint32_t box[5] = {4, (cuuint32_t)bn, 8, (cuuint32_t)nkb, 1};  // one plane, resident
         if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
             return rc;
     }
     pdl::TileParams p{};
-    p.num_kb = R;
+    p.num_kb = stem_kblocks(C, R, S);
+    p.stem_packed = stem_packed(C, R, S);
     p.seg_kb = std::max(1, kSegElems / 32);
     p.n_out = K;
     p.flags = flags;
@@ -286,12 +315,13 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     p.stride = stride;
     p.CT = 1;
     p.BW = BW;
-    p.BH = 1;
+    p.BH = BH;
     p.BNI = 1;
     p.box_w = box_w;
+    p.box_h = box_h;
     p.tiles_w = (Q + BW - 1) / BW;
-    p.tiles_h = P;
-    p.m_tiles = p.tiles_w * P * N;
+    p.tiles_h = (P + BH - 1) / BH;
+    p.m_tiles = p.tiles_w * p.tiles_h * N;
     p.n_tiles = (K + bn - 1) / bn;
     // the grid is a multiple of n_tiles: every CTA keeps one N-tile (resident weights)
     if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, 1, 1, maps, p, st);
@@ -406,7 +436,7 @@ int pdl_device_check(void) { return device_check(); }
 
 size_t pdl_conv2d_packed_bytes(int C, int K, int R, int S, unsigned flags) {
     const int planes = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 ? 2 : 1;
-    if (is_stem(C, R, S, 1)) return (size_t)planes * R * 8 * K * 4 * sizeof(float);
+    if (is_stem(C, R, S, 1)) return (size_t)planes * stem_kblocks(C, R, S) * 8 * K * 4 * sizeof(float);
     return (size_t)planes * ceil16(C) * 16 * K * R * S * sizeof(float);
 }
 
@@ -419,10 +449,11 @@ int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R
     if (!aligned16(w) || !aligned16(packed)) return fail(PDL_EALIGN, "prepack: unaligned pointer");
     const int split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     if (is_stem(C, R, S, 1)) {
-        const long long plane = (long long)R * 8 * K * 4;
+        const int nkb = stem_kblocks(C, R, S);
+        const long long plane = (long long)nkb * 8 * K * 4;
         const int blocks = (int)std::min<long long>((plane + 255) / 256, 148LL * 16);
         pdl::prepack_stem_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-            w, reinterpret_cast<float *>(packed), K, R, S, split, C);
+            w, reinterpret_cast<float *>(packed), K, R, S, split, C, nkb, stem_packed(C, R, S));
     } else {
         const long long total = (long long)K * ceil16(C) * 16 * R * S;
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);

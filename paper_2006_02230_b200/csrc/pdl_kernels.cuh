@@ -36,7 +36,8 @@ enum { KIND_GEMM = 0, KIND_CONV = 1, KIND_STEM = 2 };
 enum : unsigned {
     DBG_NO_A_TMA = 1u << 8,     // producer skips the A loads
     DBG_NO_STAGE_ST = 1u << 9,  // staging warps skip the tcgen05.st into TMEM
-    DBG_NO_EPI_STORE = 1u << 10  // epilogue skips the global stores
+    DBG_NO_EPI_STORE = 1u << 10,  // epilogue skips the global stores
+    DBG_NO_MMA = 1u << 11         // MMA warp commits without issuing the MMAs
 };
 
 // Geometry / epilogue parameters (by value, param space).
@@ -54,7 +55,8 @@ struct TileParams {
     int nimg, P, Q, KT, R, S, pad, stride, CT;
     int BW, BH, BNI;       // box of output pixels per tile
     int tiles_w, tiles_h;  // tile grid over (Q, P); images fastest-after
-    int box_w;             // stem: input pixels per halo row
+    int box_w, box_h;      // stem: halo tile (input pixels x input rows) of one output tile
+    int stem_packed;       // stem: K = (r, s, c) packed densely (C=3, 7x7), else (r, tap, c4)
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
     int raster;            // reserved
@@ -101,10 +103,13 @@ struct TmaMaps {
 //   CONV: A [CG][128 rows][16]    SW64  K-major        B [CG/2][BN rows][32] SW128 K-major
 //                                                      (CG = 1: B [BN rows][16] SW64)
 //   STEM: A [256 px][4 fp32]      halo row, no swizzle B resident: [plane][R][8 taps][BN][4]
+constexpr int kStemHaloBytes = 16384;  // stem halo tile: box_w * box_h * 16 B
+
 template <int KIND, int BN, int CG>
 struct Geo {
     static constexpr int BM = 128;
-    static constexpr int A_SUB = KIND == KIND_GEMM ? BM * 128 : KIND == KIND_CONV ? BM * 64 : 4096;
+    // stem: one stage = the whole input halo of a tile, 4 channels (16 B) per pixel
+    static constexpr int A_SUB = KIND == KIND_GEMM ? BM * 128 : KIND == KIND_CONV ? BM * 64 : kStemHaloBytes;
     // conv weights: 128-byte rows (32 input channels, SW128) whenever CG >= 2 -- 64-byte
     // SW64 rows make every tensor-core B read 2-way bank conflicted
     static constexpr int B_ROW = (KIND == KIND_CONV && CG == 1) ? 64 : 128;
@@ -280,6 +285,32 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     return c;
 }
 
+// Packed ResNet-stem gather (C=3, R=S=7): k-block KB holds K indices
+// 32KB..32KB+31 of k = (r*7 + s)*3 + c (147 real, zero beyond); one 16-byte
+// halo load per (r, s) tap, shared by the k-values it feeds.
+template <int KB>
+__device__ __forceinline__ void stem_gather_packed(uint32_t sa, uint32_t row_step, bool live,
+                                                   float (&x)[32]) {
+    constexpr int k0 = KB * 32;
+    constexpr int rs_lo = k0 / 3;
+    constexpr int rs_hi0 = (k0 + 31) / 3;
+    constexpr int rs_hi = rs_hi0 < 48 ? rs_hi0 : 48;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = 0.f;
+#pragma unroll
+    for (int rs = rs_lo; rs <= rs_hi; ++rs) {
+        const int r = rs / 7, s = rs - (rs / 7) * 7;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live) v = lds128(sa + r * row_step + s * 16);
+        const float vv[3] = {v.x, v.y, v.z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int k = rs * 3 + c - k0;
+            if (k >= 0 && k < 32) x[k] = vv[c];
+        }
+    }
+}
+
 template <int KIND, int BN, int CG, bool SPLIT3, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
@@ -361,11 +392,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             else if (KIND == KIND_CONV)
                 tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
                                 G::B_BYTES * L::LOAD_PLANES);
-            else tx = (uint32_t)(16 * p.box_w);
+            else tx = (uint32_t)(16 * p.box_w * p.box_h);
             if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
                 // resident weights of this CTA's N-tile: [plane][R][8 taps][BN][4]
                 const int n0 = (blockIdx.x % p.n_tiles) * BN;
-                mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.R * 8 * BN * 16));
+                mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.num_kb * 8 * BN * 16));
                 for (int pl = 0; pl < L::PLANES; ++pl)
                     tma_load_5d(smem + L::W_OFF + pl * (kStemMaxR * 8 * BN * 16), &maps.b, wfull, 0,
                                 n0, 0, 0, pl);
@@ -373,7 +404,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             int s = 0;
             uint32_t ph = 0;
             int kglob = 0;
-            for (int st = cid; st < num_super; st += ncl) {
+            if (KIND == KIND_STEM) {
+                // one stage = the input halo of a whole output tile; its R k-blocks
+                // (kernel rows) are all staged from it
+                for (int st = cid; st < num_super; st += ncl, ++kglob) {
+                    const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
+                    mbar_wait(&empty[s], ph ^ 1);
+                    trace_ev(p, TR_P_ISSUE, kglob);
+                    mbar_arrive_expect_tx(&full[s], tx);
+                    tma_load_5d(smem + s * L::STAGE + L::A_OFF, &maps.a[0], &full[s], 0,
+                                tc.q0 * p.stride - p.pad, tc.p0 * p.stride - p.pad, 0, tc.i0);
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+            for (int st = cid; KIND != KIND_STEM && st < num_super; st += ncl) {
                 const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
                 for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
                     mbar_wait(&empty[s], ph ^ 1);
@@ -423,10 +467,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                    &maps.b, &full[s], 0, tc.n0 + rank * SL, rs,
                                                    ctg * G::NB + nb, pl, cl_mask);
                         }
-                    } else {
-                        // stem: k-block = kernel row r; one halo row of 4-channel pixels
-                        tma_load_5d(sp + L::A_OFF, &maps.a[0], &full[s], 0,
-                                    tc.q0 * p.stride - p.pad, tc.p0 * p.stride + kb - p.pad, 0, tc.i0);
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
@@ -481,9 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             bhi = smem_desc(w, BN * 16, 128, 0);
                             blo = smem_desc(w + kStemMaxR * 8 * BN * 16, BN * 16, 128, 0);
                         }
-                        mma_ts_block<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
-                                     G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
-                            d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
+                        if (!(p.flags & DBG_NO_MMA))
+                            mma_ts_block<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
+                                         G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
+                                d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
                     } else {
 #pragma unroll
                         for (int c = 0; c < G::NSUB; ++c) {
@@ -531,7 +572,65 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= kSplitWarp0 && warp < kEpiWarp0) {
         // ===================== A staging into TMEM (hi / lo) =====================
-        if (TS) {
+        if constexpr (KIND == KIND_STEM) {
+            // thread = output pixel (ph, pw) of the BW x BH tile; k-block = kernel row r:
+            // gather taps 0..7 (4 channels each) of input row ph*stride + r from the
+            // tile's halo stage, split hi/lo, store to the TMEM A slot
+            const int tid = threadIdx.x - kSplitWarp0 * 32;
+            const int quarter = warp - kSplitWarp0;
+            const int row = quarter * 32 + lane;
+            const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+            const bool live = row < p.BW * p.BH;
+            const int ph_ = live ? row / p.BW : 0;
+            const int pw_ = live ? row - ph_ * p.BW : 0;
+            const uint32_t pix0 = (uint32_t)((ph_ * p.stride) * p.box_w + pw_ * p.stride) * 16;
+            const uint32_t row_step = (uint32_t)p.box_w * 16;
+            int s = 0, t = 0;
+            uint32_t ph = 0, tph = 0;
+            int kglob = 0;
+            const bool tr = tid == 0;
+            for (int st_i = cid; st_i < num_super; st_i += ncl) {
+                mbar_wait(&full[s], ph);
+                const uint32_t sa = smem0 + s * L::STAGE + L::A_OFF + pix0;
+                for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
+                    if (tr) trace_ev(p, TR_S_FULL, kglob);
+                    float x[32], lo[32];
+                    if (p.stem_packed) {
+                        switch (kb) {
+                            case 0: stem_gather_packed<0>(sa, row_step, live, x); break;
+                            case 1: stem_gather_packed<1>(sa, row_step, live, x); break;
+                            case 2: stem_gather_packed<2>(sa, row_step, live, x); break;
+                            case 3: stem_gather_packed<3>(sa, row_step, live, x); break;
+                            default: stem_gather_packed<4>(sa, row_step, live, x); break;
+                        }
+                    } else {
+#pragma unroll
+                        for (int tp = 0; tp < 8; ++tp) {
+                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (live && tp < p.S) v = lds128(sa + kb * row_step + tp * 16);
+                            x[4 * tp] = v.x; x[4 * tp + 1] = v.y; x[4 * tp + 2] = v.z; x[4 * tp + 3] = v.w;
+                        }
+                    }
+                    if (kb + 1 == p.num_kb) mbar_arrive(&empty[s]);  // halo tile consumed
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
+                    mbar_wait(&tfree[t], tph ^ 1);
+                    if (tr) trace_ev(p, TR_S_TFREE, kglob);
+                    tc_fence_after();
+                    const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + t * L::SLOT_COLS;
+                    if (!(p.flags & DBG_NO_STAGE_ST)) {
+                        tmem_st32(t_hi, x);
+                        if (SPLIT3) tmem_st32(t_hi + G::KS, lo);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&tready[t]);
+                    if (tr) trace_ev(p, TR_S_DONE, kglob);
+                    if (++t == TSLOTS) { t = 0; tph ^= 1; }
+                }
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+            }
+        } else if (TS) {
             const int tid = threadIdx.x - kSplitWarp0 * 32;
             const int quarter = warp - kSplitWarp0;
             const int row = quarter * 32 + lane;
@@ -592,25 +691,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tmem_st16(t_hi + c * 16, hi);
                                 if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
                             }
-                        }
-                    } else {
-                        // stem: gather taps 0..S-1 (4 channels each) of this output pixel
-                        float x[32], lo[32];
-                        const bool live = row < p.BW;
-#pragma unroll
-                        for (int tp = 0; tp < 8; ++tp) {
-                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                            if (live && tp < p.S) v = lds128(sa + (row * p.stride + tp) * 16);
-                            x[4 * tp] = v.x; x[4 * tp + 1] = v.y; x[4 * tp + 2] = v.z; x[4 * tp + 3] = v.w;
-                        }
-                        mbar_arrive(&empty[s]);  // halo row read
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
-                        mbar_wait(&tfree[t], tph ^ 1);
-                        tc_fence_after();
-                        if (!(p.flags & DBG_NO_STAGE_ST)) {
-                            tmem_st32(t_hi, x);
-                            if (SPLIT3) tmem_st32(t_hi + G::KS, lo);
                         }
                     }
                     tmem_wait_st();
@@ -852,22 +932,38 @@ __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__res
     }
 }
 
-// Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[plane][r][tap 0..7][k][4 c]
-// (no-swizzle K-major core matrices); taps >= S and channels >= C_real are zero.
+// Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[plane][kchunk][k][4]
+// (no-swizzle K-major core matrices, 4 reduction values per 16-byte chunk, 8
+// chunks per k-block).  Unpacked: chunk = r*8 + tap, value = channel (taps >= S
+// and channels >= C_real zero).  Packed (C=3, 7x7): value j of chunk kc is
+// reduction index q = 4kc + j = (r*S + s)*C + c, zero for q >= R*S*C.
 __global__ void prepack_stem_weights_kernel(const float *__restrict__ w, float *__restrict__ out,
-                                            int K, int R, int S, int split, int C_real) {
-    const long long plane = (long long)R * 8 * K * 4;
+                                            int K, int R, int S, int split, int C_real, int nkb,
+                                            int packed) {
+    const long long plane = (long long)nkb * 8 * K * 4;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
          i += (long long)gridDim.x * blockDim.x) {
-        const int c = i & 3;
+        const int j = i & 3;
         long long t = i >> 2;
         const int k = t % K;
-        t /= K;
-        const int tap = t % 8;
-        const int r = (int)(t / 8);
+        const int kc = (int)(t / K);
+        int r, tap, c;
+        bool ok;
+        if (packed) {
+            const int q = kc * 4 + j;
+            ok = q < R * S * C_real;
+            const int rs = q / C_real;
+            c = q - rs * C_real;
+            r = rs / S;
+            tap = rs - r * S;
+        } else {
+            r = kc / 8;
+            tap = kc % 8;
+            c = j;
+            ok = tap < S && c < C_real;
+        }
         float v = 0.f;
-        if (tap < S && c < C_real)
-            v = w[((((size_t)(k >> 4) * R + r) * S + tap) * 16 + c) * 16 + (k & 15)];
+        if (ok) v = w[((((size_t)(k >> 4) * R + r) * S + tap) * 16 + c) * 16 + (k & 15)];
         out[i] = v;
         if (split) out[i + plane] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     }

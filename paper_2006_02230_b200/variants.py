@@ -88,6 +88,23 @@ def stage_sizes(v: TileVariant) -> dict:
     return {"stage_bytes": stage, "stages": stages, "ks": ks, "tslots": tslots}
 
 
+def stem_tile(layer) -> tuple:
+    """BW x BH output-pixel tile of the narrow-channel stem (conv_fwd_stem in
+    csrc/pdl_capi.cu): its input halo is one TMA box / pipeline stage."""
+    P, Q, s, R, S = layer.P, layer.Q, layer.stride, layer.R, layer.S
+    best, pick = float("inf"), None
+    for bw in range(min(Q, 128), 0, -1):
+        bh = min(P, 128 // bw)
+        bxw, bxh = (bw - 1) * s + S, (bh - 1) * s + R
+        if bxw > 256 or bxh > 256 or 16 * bxw * bxh > 16384:
+            continue
+        tiles = -(-Q // bw) * -(-P // bh)
+        cost = tiles * max(R * 700.0, 4.4 * bxw * bxh)
+        if cost < best - 1e-9:
+            best, pick = cost, (bw, bh)
+    return pick
+
+
 def engine_geometry(layer, v: TileVariant, n_images: int, sms: int = 148) -> dict:
     """Tile geometry the host code picks (conv_geom in csrc/pdl_capi.cu)."""
     g = stage_sizes(v)
@@ -95,8 +112,8 @@ def engine_geometry(layer, v: TileVariant, n_images: int, sms: int = 148) -> dic
     flat = layer.R == 1 and layer.S == 1 and layer.stride == 1 and layer.pad == 0
     Pg, Qg = (1, P * Q) if flat else (P, Q)
     if _is_stem(layer):
-        bw = min(Q, 128, (256 - layer.S) // layer.stride + 1)
-        bh, bni = 1, 1
+        bw, bh = stem_tile(layer)
+        bni = 1
     else:
         bw = min(Qg, 128)
         bh = min(Pg, 128 // bw)

@@ -41,10 +41,16 @@ for arg in (sys.argv[1:] or ["3", "7", "4", "17"]):
     t0 = t[t > 0].min()
     d = {nm: [int(v - t0) if v > 0 else -1 for v in t[i]] for i, nm in enumerate(names)}
     out[l.name()] = d
-    nk = int((t[0] > 0).sum())
+    nk = int((t[3] > 0).sum())  # k-blocks staged (S_DONE); the stem has no producer loads
     def col(nm): return np.array(d[nm][:nk], dtype=np.int64)
     mr, mi, sf, sd, stf, pi = col("M_READY"), col("M_ISSUED"), col("S_FULL"), col("S_DONE"), col("S_TFREE"), col("P_ISSUE")
     total = int(mi[nk - 1])
+    print(f"  staging: S_FULL->S_TFREE median {np.median(stf - sf):.0f}, S_TFREE->S_DONE {np.median(sd - stf):.0f}, "
+          f"S_DONE->next S_FULL {np.median(sf[1:] - sd[:-1]):.0f}; per-kb S_DONE spacing {np.median(np.diff(sd)):.0f}")
+    ef, ed, es = (np.array([v for v in d[nm] if v >= 0], dtype=np.int64) for nm in ("E_FULL", "E_DRAINED", "E_STORED"))
+    if len(es) > 2:
+        print(f"  epilogue: full->drained median {np.median(ed[:len(ef)] - ef[:len(ed)]):.0f}, tiles {len(es)}, "
+              f"store spacing {np.median(np.diff(es)):.0f}")
     mma_wait = int(np.sum(np.maximum(mr[1:] - mi[:-1], 0)))
     gap = np.median(mr[1:] - mi[:-1])
     ml, mw = col("M_LOOP"), col("M_WAITED")

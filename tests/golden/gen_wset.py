@@ -78,14 +78,27 @@ CASES = [
 
 
 def _run(text, binding, q):
-    from looprank import loopdsl, wset
+    from looprank import depend, loopdsl, wset
     t = time.time()
     nest = loopdsl.parse(text)
     if nest.has_kernel_call():
         nest = loopdsl.substitute_microkernel(nest)
     rep = wset.working_sets(nest, binding)
-    q.put({"elapsed_s": round(time.time() - t, 3),
-           "entries": [[e.dep_id, e.kind, e.array, e.variant, e.elements] for e in rep.entries]})
+    elapsed = round(time.time() - t, 3)
+    info = loopdsl.extract_polyhedral(nest)
+    deps = [depend.classify_parallel_span(d, info, binding) for d in depend.compute_dependences(info)]
+    deps = [d for d in deps if d.relation.domain().lexmin(binding) is not None]  # non-empty under b
+    domains = {}
+    for st in info.statements:
+        lo, hi = st.space.lexmin(binding), st.space.lexmax(binding)
+        domains[st.label] = {"cardinality": st.space.cardinality(binding),
+                             "lexmin": None if lo is None else [int(v) for v in lo],
+                             "lexmax": None if hi is None else [int(v) for v in hi],
+                             "vars": list(st.space.vars)}
+    q.put({"elapsed_s": elapsed,
+           "entries": [[e.dep_id, e.kind, e.array, e.variant, e.elements] for e in rep.entries],
+           "deps": [[d.dep_id, d.kind, d.array, d.spans_parallel, d.parallel_iterator] for d in deps],
+           "domains": domains})
 
 
 def main():

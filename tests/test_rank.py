@@ -296,3 +296,23 @@ def test_ranker_report_committed():
     rep = json.load(open(os.path.join(os.path.dirname(__file__), "..", "profiles", "ranker_r1.json")))
     assert rep["model_loo"]["top1_regret_mean"] < rep["eq1_cost"]["top1_regret_mean"]
     assert rep["dnn_pipeline_terms"]["heldout_accuracy"] > 0.8
+
+
+# ----------------------------------------------------------------------------- R1-R3, R5
+@pytest.mark.parametrize("case", json.load(open(os.path.join(GOLD, "wset_ref.json")))["cases"],
+                         ids=lambda c: c["name"])
+def test_dependences_and_domains_match_reference(case):
+    from paper_2006_02230_b200 import depend as D
+    info = D.extract_polyhedral(parse(case["text"]))
+    b = case["binding"]
+    deps = [D.classify_parallel_span(d, info, b) for d in D.compute_dependences(info, b)]
+    assert sorted([d.dep_id, d.kind, d.array, d.spans_parallel, d.parallel_iterator] for d in deps) == \
+        sorted(case["deps"])
+    for label, dom in case["domains"].items():
+        assert D.domain_size(info, label, b) == dom["cardinality"]
+        lo, hi = D.domain_lexmin(info, label, b), D.domain_lexmax(info, label, b)
+        if dom["lexmin"] is None:
+            assert lo is None
+        else:
+            assert [lo[v] for v in dom["vars"]] == dom["lexmin"]
+            assert [hi[v] for v in dom["vars"]] == dom["lexmax"]
