@@ -385,7 +385,7 @@ class PipelineModel:
         waves = math.ceil(g["tiles"] / ctas)
         return {"num_kb": g["num_kb"], "mmas": mmas, "feed_bytes": a_bytes + b_bytes,
                 "waves": waves, "bn": variant.bn, "cluster": variant.cluster,
-                "hbm_bytes": layer.bytes(n_images) if hasattr(layer, "bytes") else 0}
+                "hbm_bytes": layer.bytes(n_images)}
 
     def predict_cycles_per_tile(self, t: dict) -> float:
         pipe = t["mmas"] * (self.mma_fixed + self.mma_per_n * t["bn"])

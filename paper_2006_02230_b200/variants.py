@@ -52,13 +52,21 @@ class VariantConfig:
     cap: int = 64
 
 
+def _is_gemm(layer) -> bool:
+    return hasattr(layer, "M") and not hasattr(layer, "R")
+
+
 def _is_stem(layer) -> bool:
-    return layer.C <= 4 and layer.S <= 8 and layer.R <= 7
+    return not _is_gemm(layer) and layer.C <= 4 and layer.S <= 8 and layer.R <= 7
 
 
 def legal(layer, v: TileVariant) -> bool:
     """Static legality: a compiled instance exists, channel grouping matches
     the packed weight rows, the stage fits shared memory / TMEM."""
+    if _is_gemm(layer):
+        # GEMM instances: bn in {64, 128}, bk = 32, cluster in {1, 2, 4}
+        return v.bk == 32 and v.bn in (64, 128) and v.cluster in (1, 2, 4) and \
+            not (v.bn > 64 and layer.N <= 64)
     if _is_stem(layer):
         return v.bn == 64 and v.cluster == 1 and v.bk == 32
     ct = (layer.C + 15) // 16
@@ -108,6 +116,13 @@ def stem_tile(layer) -> tuple:
 def engine_geometry(layer, v: TileVariant, n_images: int, sms: int = 148) -> dict:
     """Tile geometry the host code picks (conv_geom in csrc/pdl_capi.cu)."""
     g = stage_sizes(v)
+    if _is_gemm(layer):
+        m_tiles, n_tiles = -(-layer.M // 128), -(-layer.N // v.bn)
+        g.update(flat=True, bw=128, bh=1, bni=1, rows_valid=min(layer.M, 128), m_eff=1.0,
+                 m_tiles=m_tiles, n_tiles=n_tiles, tiles=m_tiles * n_tiles,
+                 num_kb=-(-layer.K // 32), seg_kb=max(1, _SEG_ELEMS // 32),
+                 tiles_concurrent=sms, tile_rows_in=1)
+        return g
     P, Q = layer.P, layer.Q
     flat = layer.R == 1 and layer.S == 1 and layer.stride == 1 and layer.pad == 0
     Pg, Qg = (1, P * Q) if flat else (P, Q)
@@ -135,7 +150,7 @@ def generate_variants(layer, cfg: VariantConfig = VariantConfig()) -> list:
     out = {}
     for mode in cfg.modes:
         for bn in cfg.bn_menu:
-            for cg in cfg.cg_menu:
+            for cg in ((2,) if _is_gemm(layer) else cfg.cg_menu):
                 for cl in cfg.cluster_menu:
                     v = TileVariant(f"bn{bn}_bk{16 * cg}_c{cl}_{mode}", bn, 16 * cg, cl, mode)
                     if legal(layer, v):
@@ -144,11 +159,15 @@ def generate_variants(layer, cfg: VariantConfig = VariantConfig()) -> list:
     if not vs:
         import warnings
         warnings.warn(f"no legal variant for {layer.name()}; using the default only")
+    if len(vs) > cfg.cap:
+        import warnings
+        warnings.warn(f"{len(vs)} variants for {layer.name()}; keeping the first {cfg.cap}")
     return vs[:cfg.cap]
 
 
 def emit_launch(v: TileVariant) -> dict:
-    """Launch configuration for the ops (`cfg=`), the B200 analogue of emit_c."""
+    """Launch configuration for the ops (`cfg=`), the B200 analogue of emit_c:
+    the fields of `pdl_tile_cfg` (include/pdl.h)."""
     return {"bm": 128, "bn": v.bn, "bk": v.bk, "cluster_m": v.cluster}
 
 

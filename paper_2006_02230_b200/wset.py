@@ -276,11 +276,22 @@ def tile_working_sets(layer, variant, n_images: int, sms: int = 148) -> WorkingS
                            running concurrently (3x3 taps)
       mem.stream           compulsory x / w / y traffic per SM
     """
-    from .variants import engine_geometry
+    from .variants import _is_gemm, engine_geometry
     g = engine_geometry(layer, variant, n_images)
     planes = 2 if variant.mode == "3xtf32" else 1
     ks = g["ks"]
     e = []
+    if _is_gemm(layer):
+        e.append(WorkingSetEntry("smem.A", "buffer", "A", "smem", g["stages"] * 128 * ks))
+        e.append(WorkingSetEntry("smem.B", "buffer", "B", "smem", g["stages"] * variant.bn * ks * planes))
+        e.append(WorkingSetEntry("tmem.acc", "buffer", "C", "tmem", 2 * 128 * variant.bn))
+        if g["tslots"]:
+            e.append(WorkingSetEntry("tmem.A", "buffer", "A", "tmem", g["tslots"] * 128 * ks * planes))
+        e.append(WorkingSetEntry("l2.Bpanel", "reuse", "B", "l2", layer.K * variant.bn))
+        e.append(WorkingSetEntry("l2.Apanel", "reuse", "A", "l2", 128 * layer.K))
+        e.append(WorkingSetEntry("mem.stream", "stream", "ABC", "mem",
+                                 int(layer.bytes() // 4 // sms)))
+        return WorkingSetReport(layer.name(), (("variant", variant.vid),), tuple(e))
     e.append(WorkingSetEntry("smem.A", "buffer", "x", "smem", g["stages"] * 128 * ks))
     e.append(WorkingSetEntry("smem.B", "buffer", "w", "smem",
                              g["stages"] * variant.bn * ks * planes))
