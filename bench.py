@@ -37,7 +37,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="suite", choices=["suite", "gemm", "pr1"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "gemm", "pr1", "layout"])
     ap.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--batch", type=int, default=256, help="global minibatch (suite)")
     ap.add_argument("--unfused", action="store_true", help="also time conv + separate bias/ReLU")
@@ -484,6 +484,57 @@ def run_gemm(args, rank, world, local):
             "gemms": rows, "gpu_launches": len(rows) * args.steps}
 
 
+def run_layout(args, rank, world, local):
+    """Data path either side of the conv: NCHW -> nChw16c pack of
+    the network input and nChw16c -> NCHW unpack of the largest activation at
+    batch 256; HBM-bound, algorithmic bytes = read + write."""
+    import torch
+    import paper_2006_02230_b200 as P
+    torch.cuda.set_device(local)
+    peaks = load_peaks()
+    n = args.batch
+    cases = [("pack_nchw16c stem input", "pack", (n, 3, 224, 224)),
+             ("pack_nchw16c 64x56x56", "pack", (n, 64, 56, 56)),
+             ("unpack_nchw16c 256x56x56", "unpack", (n, 256, 56, 56)),
+             ("unpack_nchw16c 2048x7x7", "unpack", (n, 2048, 7, 7))]
+    stream = torch.cuda.current_stream()
+    rows, tot_b, tot_ms = [], 0, 0.0
+    for name, kind, (N, C, H, Wd) in cases:
+        cb = (C + 15) // 16
+        nchw = torch.rand((N, C, H, Wd), device="cuda")
+        blk = torch.empty((N, cb, H, Wd, 16), device="cuda")
+        if kind == "unpack":
+            P.to_nchw16c(nchw, out=blk)
+        run = (lambda: P.to_nchw16c(nchw, out=blk)) if kind == "pack" else \
+            (lambda: P.from_nchw16c(blk, C, out=nchw))
+        for _ in range(args.warmup):
+            run()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        nbytes = 4 * N * C * H * Wd + 4 * N * cb * 16 * H * Wd
+        rows.append({"case": name, "ms": round(ms, 4), "gbs": round(nbytes / ms / 1e6, 1),
+                     "roofline_frac": round(nbytes / ms / 1e6 / peaks["hbm_gbs"], 3)})
+        tot_b += nbytes
+        tot_ms += ms
+    gbs = tot_b / tot_ms / 1e6
+    return {"metric": "NCHW<->nChw16c pack/unpack GB/s", "value": round(gbs, 1), "unit": "GB/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms, 4),
+            "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic U[0,1)",
+            "config": {"workload": "layout_pack_unpack", "batch": n,
+                       "l2": "every tensor >> 126 MB L2 except 2048x7x7 (102 MB)"},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
+                         "kernel": "pack_nchw16c_kernel / unpack_nchw16c_kernel", "traffic": None},
+            "cases": rows, "gpu_launches": len(rows) * (args.steps + args.warmup)}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     """The reference's CPU implementation of the path = the oracle port of the
@@ -528,6 +579,8 @@ def main():
         out = run_suite(args, rank, world, local)
     elif args.workload == "gemm":
         out = run_gemm(args, rank, world, local) if rank == 0 else None
+    elif args.workload == "layout":
+        out = run_layout(args, rank, world, local) if rank == 0 else None
     else:
         args.batch = 1
         out = run_suite_pr1(args, rank, world, local) if rank == 0 else None

@@ -52,10 +52,10 @@ extern "C" {
  * NULL or zero fields = library default.  bm is fixed at 128 (tcgen05 M). */
 typedef struct pdl_tile_cfg {
     int bm;        /* output rows (pixels / GEMM M) per CTA tile: 128          */
-    int bn;        /* output columns (K channels / GEMM N) per tile: 64|128|256 */
+    int bn;        /* output columns (K channels / GEMM N) per tile: 64|128     */
     int bk;        /* reduction elements per pipeline stage (16*cg for conv)    */
     int stages;    /* smem pipeline depth                                       */
-    int cluster_m; /* reserved (1)                                              */
+    int cluster_m; /* CTAs per cluster sharing (TMA-multicasting) a weight tile: 1|2|4 */
     int cluster_n; /* reserved (1)                                              */
     int split_k;   /* reserved (1)                                              */
     int raster;    /* 0: M-tiles fastest, 1: N-tiles fastest                    */
@@ -108,6 +108,15 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
 /* Unfused element-wise pass over y[N][K/16][P][Q][16] (the GPU baseline). */
 int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int Q,
                           unsigned flags, void *stream);
+
+/* Layout conversion on either side of the path (device to device):
+ *   NCHW [N][C][H][W]      <-> nChw16c [N][ceil(C/16)][H][W][16] (pad channels zero)
+ *   OIHW [K][C][R][S]       -> KCRS16c16k [K/16][ceil(C/16)][R][S][16c][16k]
+ * The reference keeps tensors blocked throughout; these are
+ * the pack/unpack steps a PyTorch-layout caller needs before/after it. */
+int pdl_pack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream);
+int pdl_unpack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream);
+int pdl_pack_kcrs16c16k(const float *src, float *dst, int K, int C, int R, int S, void *stream);
 
 size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg);
 

@@ -31,7 +31,8 @@ EXPORTS = (
     "pdl_conv2d_fwd_nchw16c", "pdl_conv2d_packed_bytes", "pdl_conv2d_prepack_weights",
     "pdl_conv2d_fwd_prepacked", "pdl_gemm_f32", "pdl_bias_relu_nchw16c",
     "pdl_workspace_bytes", "pdl_default_cfg", "pdl_last_launch_count", "pdl_last_error",
-    "pdl_abi_version", "pdl_device_check",
+    "pdl_abi_version", "pdl_device_check", "pdl_pack_nchw16c", "pdl_unpack_nchw16c",
+    "pdl_pack_kcrs16c16k",
 )
 
 
@@ -86,6 +87,9 @@ def _declare(L):
     L.pdl_gemm_f32.argtypes = [_vp, _vp, _vp] + [_i] * 6 + [
         ctypes.c_float, ctypes.c_float, _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
     L.pdl_bias_relu_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
+    L.pdl_pack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
+    L.pdl_unpack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
+    L.pdl_pack_kcrs16c16k.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_workspace_bytes.argtypes = [_i, ctypes.POINTER(_i), ctypes.POINTER(TileCfg)]
     L.pdl_workspace_bytes.restype = _sz
     L.pdl_default_cfg.argtypes = [_i, ctypes.POINTER(_i), ctypes.POINTER(TileCfg)]

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "../../include/pdl.h"
+#include "pdl_layout.cuh"
 #include "pdl_kernels.cuh"
 
 namespace {
@@ -236,6 +237,16 @@ void conv_default_cfg(int C, int K, pdl_tile_cfg *c) {
     c->raster = 0;
 }
 
+// Output map of the TMA-stored epilogue: y [N][KT][Pg][Qg][16] in the tile
+// geometry (flattened for 1x1/s1/p0), box = one 16-channel block of a tile.
+int encode_y(CUtensorMap *m, float *y, int N, int KT, int Pg, int Qg, int BW, int BH, int BNI) {
+    const cuuint64_t dims[5] = {16, (cuuint64_t)Qg, (cuuint64_t)Pg, (cuuint64_t)KT, (cuuint64_t)N};
+    const cuuint64_t str[4] = {64, (cuuint64_t)Qg * 64, (cuuint64_t)Pg * Qg * 64,
+                               (cuuint64_t)KT * Pg * Qg * 64};
+    const cuuint32_t box[5] = {16, (cuuint32_t)BW, (cuuint32_t)BH, 1, (cuuint32_t)BNI};
+    return encode(m, y, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B, "conv y");
+}
+
 int conv_check(const float *x, const float *y, int N, int C, int K, int H, int W, int R, int S,
                int stride, int pad) {
     if (N <= 0 || C <= 0 || K <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0)
@@ -297,6 +308,7 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
         if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
             return rc;
     }
+    if ((rc = encode_y(&maps.y, y, N, K / 16, P, Q, BW, BH, 1))) return rc;
     pdl::TileParams p{};
     p.num_kb = stem_kblocks(C, R, S);
     p.stem_packed = stem_packed(C, R, S);
@@ -391,6 +403,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                          G == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
             return rc;
     }
+    if ((rc = encode_y(&maps.y, y, N, KT, g.Pg, g.Qg, g.BW, g.BH, g.BNI))) return rc;
     pdl::TileParams p{};
     p.num_kb = (CT / cg) * R * S;
     p.seg_kb = std::max(1, kSegElems / (16 * cg));
@@ -590,6 +603,57 @@ int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int 
         reinterpret_cast<float4 *>(y), reinterpret_cast<const float4 *>(bias), n4, P * Q, K / 16, flags);
     ++g_launches;
     return check_launch("bias_relu_kernel");
+}
+
+static int layout_check(const void *a, const void *b, long long n) {
+    int rc;
+    if ((rc = device_check())) return rc;
+    if (n < 0) return fail(PDL_EINVAL, "layout: negative dimension");
+    if (!a || !b) return fail(PDL_EINVAL, "layout: null pointer");
+    return PDL_OK;
+}
+
+int pdl_pack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = layout_check(src, dst, (long long)N | C | H | W))) return rc;
+    if (N <= 0 || C <= 0 || H <= 0 || W <= 0) return fail(PDL_EINVAL, "pack: empty tensor");
+    if (!aligned16(dst)) return fail(PDL_EALIGN, "pack: dst must be 16-byte aligned");
+    const long long planes = (long long)N * ceil16(C), hw = (long long)H * W;
+    if (planes > 65535 || (hw + 255) / 256 > 0x7fffffffLL)
+        return fail(PDL_EUNSUPPORTED, "pack: tensor too large");
+    const dim3 grid((unsigned)((hw + pdl::kLayoutThreads - 1) / pdl::kLayoutThreads), (unsigned)planes);
+    pdl::pack_nchw16c_kernel<<<grid, pdl::kLayoutThreads, 0, (cudaStream_t)stream>>>(src, dst, N, C, H, W);
+    ++g_launches;
+    return check_launch("pack_nchw16c_kernel");
+}
+
+int pdl_unpack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = layout_check(src, dst, (long long)N | C | H | W))) return rc;
+    if (N <= 0 || C <= 0 || H <= 0 || W <= 0) return fail(PDL_EINVAL, "unpack: empty tensor");
+    if (!aligned16(src)) return fail(PDL_EALIGN, "unpack: src must be 16-byte aligned");
+    const long long planes = (long long)N * ceil16(C), hw = (long long)H * W;
+    if (planes > 65535 || (hw + 255) / 256 > 0x7fffffffLL)
+        return fail(PDL_EUNSUPPORTED, "unpack: tensor too large");
+    const dim3 grid((unsigned)((hw + pdl::kLayoutThreads - 1) / pdl::kLayoutThreads), (unsigned)planes);
+    pdl::unpack_nchw16c_kernel<<<grid, pdl::kLayoutThreads, 0, (cudaStream_t)stream>>>(src, dst, N, C, H, W);
+    ++g_launches;
+    return check_launch("unpack_nchw16c_kernel");
+}
+
+int pdl_pack_kcrs16c16k(const float *src, float *dst, int K, int C, int R, int S, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = layout_check(src, dst, (long long)K | C | R | S))) return rc;
+    if (K <= 0 || K % 16 || C <= 0 || R <= 0 || S <= 0)
+        return fail(PDL_EINVAL, "pack weights: K must be a positive multiple of 16");
+    const long long total = (long long)K * ceil16(C) * 16 * R * S;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    pdl::pack_kcrs16c16k_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(src, dst, K, C, R, S);
+    ++g_launches;
+    return check_launch("pack_kcrs16c16k_kernel");
 }
 
 size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg) {

@@ -96,6 +96,7 @@ __device__ __forceinline__ void trace_ev(const TileParams &p, int ev, int i) {
 struct TmaMaps {
     CUtensorMap a[4];  // conv: one per (row, col) parity for stride 2; GEMM / stem: a[0]
     CUtensorMap b;
+    CUtensorMap y;     // conv / stem output [N][KT][P][Q][16] (TMA-stored epilogue)
 };
 
 // Shared-memory tiles of one pipeline stage.
@@ -146,7 +147,10 @@ struct Smem {
     // stem weights stay resident for the whole kernel (one N-tile per CTA)
     static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * kStemMaxR * 8 * BN * 16 : 0;
     static constexpr int STAGE = KIND == KIND_STEM ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
-    static constexpr int BUDGET = 216 * 1024 - W_BYTES;
+    // conv / stem epilogue: one 128-row x 16-channel (8 KB, SW64) TMA-store buffer
+    // per column half of the epilogue warps
+    static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * 8192;
+    static constexpr int BUDGET = 216 * 1024 - W_BYTES - EPI_BYTES;
     static constexpr int S0 = BUDGET / STAGE;
     static constexpr int STAGES = S0 > 16 ? 16 : S0;
     static constexpr int SLOT_COLS = SPLIT3 ? 2 * G::KS : G::KS;  // TMEM columns per A slot
@@ -157,7 +161,8 @@ struct Smem {
     static constexpr int B_HI = G::A_BYTES;
     static constexpr int B_LO = B_HI + G::B_BYTES;
     static constexpr int W_OFF = STAGES * STAGE;       // stem weights
-    static constexpr int BAR_OFF = W_OFF + W_BYTES;
+    static constexpr int EPI_OFF = W_OFF + W_BYTES;
+    static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
     static constexpr int TOTAL = BAR_OFF + 1024 + 1024;  // barriers + alignment slack
     static constexpr uint32_t TMEM_COLS = TS ? 512 : 2 * BN;
     static_assert(STAGES >= 2, "tile too large for a 2-stage pipeline");
@@ -740,6 +745,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(&tmem_empty[g & 1]);
                 if (tr) trace_ev(p, TR_E_DRAINED, g);
             }
+            if constexpr (KIND != KIND_GEMM) {
+                // ---- store via TMA (bias + ReLU fused): per 16-channel block, the half's
+                // 128 threads write their pixel's 64 bytes into a SW64 smem image of the
+                // output box, one thread stores the box; TMA clips pixels outside P x Q
+                const uint32_t ebuf = smem0 + L::EPI_OFF + half * 8192;
+                const bool in_box = row < p.BW * p.BH * p.BNI;
+                const bool leader = quarter == 0 && lane == 0;
+                const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
+                const bool relu = p.flags & PDL_RELU;
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    const int col0 = tc.n0 + half * HALF + j * 16;
+                    if (leader) bulk_wait_read<0>();  // previous box left the buffer
+                    named_bar_sync(2 + half, 128);
+                    if (in_box) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            float4 r = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
+                                                   sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
+                            if (has_bias && col0 < p.n_out) {
+                                const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col0 + q4 * 4));
+                                r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+                            }
+                            if (relu) {
+                                r.x = (0.f > r.x) ? 0.f : r.x;
+                                r.y = (0.f > r.y) ? 0.f : r.y;
+                                r.z = (0.f > r.z) ? 0.f : r.z;
+                                r.w = (0.f > r.w) ? 0.f : r.w;
+                            }
+                            sts128(ebuf + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4), r);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(2 + half, 128);
+                    if (leader && col0 < p.n_out && !(p.flags & DBG_NO_EPI_STORE)) {
+                        tma_store_5d(&maps.y, ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
+                        bulk_commit();
+                    }
+                }
+                if (tr) trace_ev(p, TR_E_STORED, jt);
+                continue;
+            }
             // ---- store (bias + ReLU fused) ----
             bool valid;
             float *obase;
@@ -775,6 +822,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tr) trace_ev(p, TR_E_STORED, jt);
         }
     }
+    if (KIND != KIND_GEMM && warp >= kEpiWarp0 && ((warp - kEpiWarp0) & 3) == 0 && lane == 0)
+        bulk_wait<0>();  // output boxes written before the CTA retires
     __syncwarp();
     tc_fence_before();
     if (CL > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it

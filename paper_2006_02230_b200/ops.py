@@ -165,6 +165,52 @@ def bias_relu_(y: torch.Tensor, bias: torch.Tensor | None, relu: bool = True,
     return y
 
 
+def to_nchw16c(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """NCHW -> nChw16c (channels padded with zeros to a multiple of 16)."""
+    x = x.contiguous()
+    _need_cuda_f32("x", x)
+    n, c, h, w = x.shape
+    if out is None:
+        out = torch.empty((n, (c + 15) // 16, h, w, 16), dtype=torch.float32, device=x.device)
+    check(lib().pdl_pack_nchw16c(_ptr(x), _ptr(out), n, c, h, w, ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def from_nchw16c(y: torch.Tensor, channels: int | None = None, out: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+    """nChw16c -> NCHW, dropping padding channels beyond `channels`."""
+    _need_cuda_f32("y", y)
+    n, cb, h, w, v = y.shape
+    c = channels if channels is not None else cb * 16
+    if out is None:
+        out = torch.empty((n, c, h, w), dtype=torch.float32, device=y.device)
+    check(lib().pdl_unpack_nchw16c(_ptr(y), _ptr(out), n, c, h, w, ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def weights_to_kcrs16c16k(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """OIHW [K][C][R][S] -> KCRS16c16k (input channels padded with zeros)."""
+    w = w.contiguous()
+    _need_cuda_f32("w", w)
+    k, c, r, s = w.shape
+    out = torch.empty((k // 16, (c + 15) // 16, r, s, 16, 16), dtype=torch.float32, device=w.device)
+    check(lib().pdl_pack_kcrs16c16k(_ptr(w), _ptr(out), k, c, r, s, ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def conv2d_nchw(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, stride: int = 1,
+                pad: int = 0, relu: bool = False, mode: str = "3xtf32", cfg=None,
+                stream=None) -> torch.Tensor:
+    """PyTorch-layout convenience: NCHW x, OIHW w -> NCHW y, through pack ->
+    blocked conv (+bias, +ReLU) -> unpack; all on the GPU."""
+    c = x.shape[1]
+    xb = to_nchw16c(x, stream=stream)
+    pw = prepack_weights(weights_to_kcrs16c16k(w, stream=stream), mode=mode, channels=c, stream=stream)
+    yb = conv2d_nchw16c(xb, pw, bias, stride=stride, pad=pad, relu=relu, mode=mode, cfg=cfg,
+                        channels=c, stream=stream)
+    return from_nchw16c(yb, w.shape[0], stream=stream)
+
+
 def device_ok() -> bool:
     return lib().pdl_device_check() == 0
 
