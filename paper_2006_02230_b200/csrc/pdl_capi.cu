@@ -146,7 +146,9 @@ template <int KIND, bool SPLIT3, int CL>
 int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, int work,
                 cudaStream_t s) {
     if constexpr (KIND == pdl::KIND_STEM) {
-        if (bn == 64 && CL == 1) return launch_tile<KIND, 64, 1, SPLIT3, 1>(maps, p, work, s);
+        if (bn == 64 && CL == 1 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3, 1>(maps, p, work, s);
+        if (bn == 64 && CL == 1 && cg == pdl::kStemPackedCG)
+            return launch_tile<KIND, 64, pdl::kStemPackedCG, SPLIT3, 1>(maps, p, work, s);
     } else if constexpr (KIND == pdl::KIND_GEMM) {
         switch (bn) {
             case 64: return launch_tile<KIND, 64, 1, SPLIT3, CL>(maps, p, work, s);
@@ -212,14 +214,13 @@ bool is_stem(int C, int R, int S, int stride) {
 
 int ceil16(int c) { return (c + 15) / 16; }
 
-// ResNet stem (C=3, 7x7) can pack (r, s, c) densely along K (147 -> 5 k-blocks
-// of 32) instead of one k-block of 8 taps x 4 channels per kernel row (7
-// k-blocks, 224): 29% fewer MMAs, but the gather then needs ~11 halo loads per
-// k-block and measured 0.60 ms vs 0.50 ms unpacked at N=256 (the stem is
-// staging/TMA-bound, not MMA-bound).  Kept selectable for the ranker; off.
-bool g_stem_pack = false;
-bool stem_packed(int C, int R, int S) { return g_stem_pack && C == 3 && R == 7 && S == 7; }
-int stem_kblocks(int C, int R, int S) { return stem_packed(C, R, S) ? (R * S * C + 31) / 32 : R; }
+// ResNet stem (C=3, 7x7): the reduction is packed (r, s, c)-dense, 147 -> 160
+// values in two k-blocks of 80 (20 four-value chunks each) instead of one
+// k-block of 8 taps x 4 channels per kernel row (7 x 32 = 224): 29% fewer MMAs
+// and 2 instead of 7 MMA-warp passes per tile.  Other narrow shapes keep rows.
+bool stem_packed(int C, int R, int S) { return C == 3 && R == 7 && S == 7; }
+int stem_kblocks(int C, int R, int S) { return stem_packed(C, R, S) ? 2 : R; }
+int stem_chunks_per_kb(int C, int R, int S) { return stem_packed(C, R, S) ? 20 : 8; }
 
 // Input channels per packed weight row: 32 (128-byte SW128 rows) when the number
 // of 16-channel blocks is even, else 16 (64-byte SW64 rows).
@@ -300,19 +301,18 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     }
     {
         const int planes = split ? 2 : 1;
-        const int nkb = stem_kblocks(C, R, S);
-        const cuuint64_t dims[5] = {4, (cuuint64_t)K, 8, (cuuint64_t)nkb, (cuuint64_t)planes};
-        const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)8 * K * 16,
-                                   (cuuint64_t)nkb * 8 * K * 16};
-        const cuuint32_t box[5] = {4, (cuuint32_t)bn, 8, (cuuint32_t)nkb, 1};  // one plane, resident
+        const int nkb = stem_kblocks(C, R, S), cpk = stem_chunks_per_kb(C, R, S);
+        const cuuint64_t dims[5] = {4, (cuuint64_t)K, (cuuint64_t)cpk, (cuuint64_t)nkb, (cuuint64_t)planes};
+        const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)cpk * K * 16,
+                                   (cuuint64_t)nkb * cpk * K * 16};
+        const cuuint32_t box[5] = {4, (cuuint32_t)bn, (cuuint32_t)cpk, (cuuint32_t)nkb, 1};  // resident
         if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
             return rc;
     }
     if ((rc = encode_y(&maps.y, y, N, K / 16, P, Q, BW, BH, 1))) return rc;
     pdl::TileParams p{};
     p.num_kb = stem_kblocks(C, R, S);
-    p.stem_packed = stem_packed(C, R, S);
-    p.seg_kb = std::max(1, kSegElems / 32);
+    p.seg_kb = std::max(1, kSegElems / (4 * stem_chunks_per_kb(C, R, S)));
     p.n_out = K;
     p.flags = flags;
     p.bias = bias;
@@ -336,8 +336,9 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     p.m_tiles = p.tiles_w * p.tiles_h * N;
     p.n_tiles = (K + bn - 1) / bn;
     // the grid is a multiple of n_tiles: every CTA keeps one N-tile (resident weights)
-    if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, 1, 1, maps, p, st);
-    return dispatch_tile<pdl::KIND_STEM, false>(bn, 1, 1, maps, p, st);
+    const int scg = stem_packed(C, R, S) ? pdl::kStemPackedCG : 1;
+    if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, scg, 1, maps, p, st);
+    return dispatch_tile<pdl::KIND_STEM, false>(bn, scg, 1, maps, p, st);
 }
 
 int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, int N, int C, int K,
@@ -449,7 +450,8 @@ int pdl_device_check(void) { return device_check(); }
 
 size_t pdl_conv2d_packed_bytes(int C, int K, int R, int S, unsigned flags) {
     const int planes = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 ? 2 : 1;
-    if (is_stem(C, R, S, 1)) return (size_t)planes * stem_kblocks(C, R, S) * 8 * K * 4 * sizeof(float);
+    if (is_stem(C, R, S, 1))
+        return (size_t)planes * stem_kblocks(C, R, S) * stem_chunks_per_kb(C, R, S) * K * 4 * sizeof(float);
     return (size_t)planes * ceil16(C) * 16 * K * R * S * sizeof(float);
 }
 
@@ -462,11 +464,11 @@ int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R
     if (!aligned16(w) || !aligned16(packed)) return fail(PDL_EALIGN, "prepack: unaligned pointer");
     const int split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     if (is_stem(C, R, S, 1)) {
-        const int nkb = stem_kblocks(C, R, S);
-        const long long plane = (long long)nkb * 8 * K * 4;
+        const int nch = stem_kblocks(C, R, S) * stem_chunks_per_kb(C, R, S);
+        const long long plane = (long long)nch * K * 4;
         const int blocks = (int)std::min<long long>((plane + 255) / 256, 148LL * 16);
         pdl::prepack_stem_weights_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-            w, reinterpret_cast<float *>(packed), K, R, S, split, C, nkb, stem_packed(C, R, S));
+            w, reinterpret_cast<float *>(packed), K, R, S, split, C, nch, stem_packed(C, R, S));
     } else {
         const long long total = (long long)K * ceil16(C) * 16 * R * S;
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);

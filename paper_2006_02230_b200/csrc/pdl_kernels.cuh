@@ -56,7 +56,6 @@ struct TileParams {
     int BW, BH, BNI;       // box of output pixels per tile
     int tiles_w, tiles_h;  // tile grid over (Q, P); images fastest-after
     int box_w, box_h;      // stem: halo tile (input pixels x input rows) of one output tile
-    int stem_packed;       // stem: K = (r, s, c) packed densely (C=3, 7x7), else (r, tap, c4)
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
     int raster;            // reserved
@@ -103,8 +102,13 @@ struct TmaMaps {
 //   GEMM: A [128 rows][32 fp32]   SW128 K-major        B [BN/32][32 k][32 n] SW128_B32 MN-major
 //   CONV: A [CG][128 rows][16]    SW64  K-major        B [CG/2][BN rows][32] SW128 K-major
 //                                                      (CG = 1: B [BN rows][16] SW64)
-//   STEM: A [256 px][4 fp32]      halo row, no swizzle B resident: [plane][R][8 taps][BN][4]
+//   STEM: A halo tile [rows][px][4 fp32], no swizzle   B resident: [plane][chunk][BN][4]
 constexpr int kStemHaloBytes = 16384;  // stem halo tile: box_w * box_h * 16 B
+// For KIND_STEM the CG template parameter selects the reduction packing:
+//   CG = 1: k-block = one kernel row, K = 8 taps x 4 channels = 32 (any C <= 4, S <= 8)
+//   CG = kStemPackedCG: K = (r, s, c) dense for C = 3, 7x7 (147 -> 160), two k-blocks of
+//           80 per tile (one TMEM slot each): 29% fewer MMAs and 5 MMA-warp passes -> 2
+constexpr int kStemPackedCG = 5;
 
 template <int KIND, int BN, int CG>
 struct Geo {
@@ -120,17 +124,25 @@ struct Geo {
     static constexpr int A_BYTES = A_SUB * NSUB;
     static constexpr int B_BYTES = B_SUB * NB;
     static constexpr int KK = KIND == KIND_CONV ? 2 : 4;  // K=8 MMAs per sub-tile
-    static constexpr int KS = KIND == KIND_CONV ? 16 * CG : 32;  // K elements per stage
+    static constexpr bool STEM_PACKED = KIND == KIND_STEM && CG == kStemPackedCG;
+    static constexpr int KS = KIND == KIND_CONV ? 16 * CG : STEM_PACKED ? 80 : 32;  // K per k-block
     static constexpr int NK = KS / 8;                                // K=8 MMA steps per stage
     // B-descriptor advance (16-byte units) of K=8 step j within a stage
     __host__ __device__ static constexpr uint32_t boff(int j) {
         return KIND == KIND_GEMM ? (uint32_t)(j * 64)                   // 8 k-rows x 128 B
              : KIND == KIND_CONV ? (uint32_t)(((j * 32) / B_ROW * B_SUB + (j * 32) % B_ROW) / 16)
-                                 : (uint32_t)(j * 2 * BN);             // stem: 2 taps x BN x 16 B
+                                 : (uint32_t)(j * 2 * BN);             // stem: 2 chunks x BN x 16 B
     }
 };
 
 constexpr int kStemMaxR = 7;  // resident stem weights: R <= 7 kernel rows
+
+// one plane of the stem's resident weights: (k-blocks x KS/4 chunks) x BN x 16 B
+template <int BN, int CG>
+struct StemW {
+    static constexpr int CHUNKS = CG == kStemPackedCG ? 2 * 20 : kStemMaxR * 8;
+    static constexpr int PLANE_BYTES = CHUNKS * BN * 16;
+};
 
 // TS = A operand staged in TMEM by the split warps (3xTF32, and the stem's tap gather).
 // SMEM stages (TMA ring) and TMEM A slots (split -> MMA ring) are separate rings.
@@ -145,7 +157,7 @@ struct Smem {
     // staging warps' smem traffic costs more than the TMA bytes it saves.)
     static constexpr int LOAD_PLANES = KIND == KIND_GEMM ? 1 : PLANES;
     // stem weights stay resident for the whole kernel (one N-tile per CTA)
-    static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * kStemMaxR * 8 * BN * 16 : 0;
+    static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * StemW<BN, CG>::PLANE_BYTES : 0;
     static constexpr int STAGE = KIND == KIND_STEM ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
     // conv / stem epilogue: one 128-row x 16-channel (8 KB, SW64) TMA-store buffer
     // per column half of the epilogue warps
@@ -290,18 +302,17 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     return c;
 }
 
-// Packed ResNet-stem gather (C=3, R=S=7): k-block KB holds K indices
-// 32KB..32KB+31 of k = (r*7 + s)*3 + c (147 real, zero beyond); one 16-byte
-// halo load per (r, s) tap, shared by the k-values it feeds.
-template <int KB>
-__device__ __forceinline__ void stem_gather_packed(uint32_t sa, uint32_t row_step, bool live,
-                                                   float (&x)[32]) {
-    constexpr int k0 = KB * 32;
-    constexpr int rs_lo = k0 / 3;
-    constexpr int rs_hi0 = (k0 + 31) / 3;
+// Packed ResNet-stem gather (C=3, R=S=7): reduction index k = (r*7 + s)*3 + c
+// (147 real, zero beyond).  Values K0..K0+15: one 16-byte halo load per (r, s)
+// tap, shared by the k-values it feeds; everything is compile-time but the
+// halo addresses.
+template <int K0>
+__device__ __forceinline__ void stem_gather16(uint32_t sa, uint32_t row_step, bool live, float (&x)[16]) {
+    constexpr int rs_lo = K0 / 3;
+    constexpr int rs_hi0 = (K0 + 15) / 3;
     constexpr int rs_hi = rs_hi0 < 48 ? rs_hi0 : 48;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = 0.f;
+    for (int i = 0; i < 16; ++i) x[i] = 0.f;
 #pragma unroll
     for (int rs = rs_lo; rs <= rs_hi; ++rs) {
         const int r = rs / 7, s = rs - (rs / 7) * 7;
@@ -310,9 +321,21 @@ __device__ __forceinline__ void stem_gather_packed(uint32_t sa, uint32_t row_ste
         const float vv[3] = {v.x, v.y, v.z};
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const int k = rs * 3 + c - k0;
-            if (k >= 0 && k < 32) x[k] = vv[c];
+            const int k = rs * 3 + c - K0;
+            if (k >= 0 && k < 16) x[k] = vv[c];
         }
+    }
+}
+// chunk c (0..4) of packed k-block KB (80 values each)
+template <int KB>
+__device__ __forceinline__ void stem_gather16_kb(int c, uint32_t sa, uint32_t row_step, bool live,
+                                                 float (&x)[16]) {
+    switch (c) {
+        case 0: stem_gather16<KB * 80 + 0>(sa, row_step, live, x); break;
+        case 1: stem_gather16<KB * 80 + 16>(sa, row_step, live, x); break;
+        case 2: stem_gather16<KB * 80 + 32>(sa, row_step, live, x); break;
+        case 3: stem_gather16<KB * 80 + 48>(sa, row_step, live, x); break;
+        default: stem_gather16<KB * 80 + 64>(sa, row_step, live, x); break;
     }
 }
 
@@ -399,11 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 G::B_BYTES * L::LOAD_PLANES);
             else tx = (uint32_t)(16 * p.box_w * p.box_h);
             if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
-                // resident weights of this CTA's N-tile: [plane][R][8 taps][BN][4]
+                // resident weights of this CTA's N-tile: [plane][kb][KS/4 chunks][BN][4]
                 const int n0 = (blockIdx.x % p.n_tiles) * BN;
-                mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.num_kb * 8 * BN * 16));
+                mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.num_kb * (G::KS / 4) * BN * 16));
                 for (int pl = 0; pl < L::PLANES; ++pl)
-                    tma_load_5d(smem + L::W_OFF + pl * (kStemMaxR * 8 * BN * 16), &maps.b, wfull, 0,
+                    tma_load_5d(smem + L::W_OFF + pl * StemW<BN, CG>::PLANE_BYTES, &maps.b, wfull, 0,
                                 n0, 0, 0, pl);
             }
             int s = 0;
@@ -521,15 +544,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                             blo = smem_desc(st + L::B_LO, 16, 8 * G::B_ROW, lay);
                         } else {
                             // resident no-swizzle K-major weights: 8-row x 16B core matrices;
-                            // taps (2j, 2j+1) are BN*16 B apart
-                            const uint32_t w = smem0 + L::W_OFF + (uint32_t)(kb * 8 * BN * 16);
+                            // 4-value chunks (2j, 2j+1) are BN*16 B apart
+                            const uint32_t w = smem0 + L::W_OFF + (uint32_t)(kb * (G::KS / 4) * BN * 16);
                             bhi = smem_desc(w, BN * 16, 128, 0);
-                            blo = smem_desc(w + kStemMaxR * 8 * BN * 16, BN * 16, 128, 0);
+                            blo = smem_desc(w + StemW<BN, CG>::PLANE_BYTES, BN * 16, 128, 0);
                         }
-                        if (!(p.flags & DBG_NO_MMA))
+                        if (p.flags & DBG_NO_MMA) {
+                        } else if constexpr (G::NK == 10) {  // packed stem: 8 + 2 k-steps
+                            mma_ts_block<8, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2), G::boff(3),
+                                         G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
+                                d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
+                            mma_ts_block<2, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2), G::boff(3)>(
+                                d_tmem, a_t + 64, bhi + G::boff(8), blo + G::boff(8), idesc, 1u);
+                        } else {
                             mma_ts_block<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
                                          G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
                                 d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
+                        }
                     } else {
 #pragma unroll
                         for (int c = 0; c < G::NSUB; ++c) {
@@ -599,22 +630,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t sa = smem0 + s * L::STAGE + L::A_OFF + pix0;
                 for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
                     if (tr) trace_ev(p, TR_S_FULL, kglob);
-                    float x[32], lo[32];
-                    if (p.stem_packed) {
-                        switch (kb) {
-                            case 0: stem_gather_packed<0>(sa, row_step, live, x); break;
-                            case 1: stem_gather_packed<1>(sa, row_step, live, x); break;
-                            case 2: stem_gather_packed<2>(sa, row_step, live, x); break;
-                            case 3: stem_gather_packed<3>(sa, row_step, live, x); break;
-                            default: stem_gather_packed<4>(sa, row_step, live, x); break;
-                        }
-                    } else {
+                    if constexpr (G::STEM_PACKED) {
+                        // 80 packed reduction values = 5 chunks of 16, gathered and stored
+                        // chunk by chunk (registers stay at 2 x 16)
+                        mbar_wait(&tfree[t], tph ^ 1);
+                        if (tr) trace_ev(p, TR_S_TFREE, kglob);
+                        tc_fence_after();
+                        const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + t * L::SLOT_COLS;
 #pragma unroll
-                        for (int tp = 0; tp < 8; ++tp) {
-                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                            if (live && tp < p.S) v = lds128(sa + kb * row_step + tp * 16);
-                            x[4 * tp] = v.x; x[4 * tp + 1] = v.y; x[4 * tp + 2] = v.z; x[4 * tp + 3] = v.w;
+                        for (int c = 0; c < 5; ++c) {
+                            float x[16], lo[16];
+                            if (kb == 0) stem_gather16_kb<0>(c, sa, row_step, live, x);
+                            else stem_gather16_kb<1>(c, sa, row_step, live, x);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) lo[i] = tf32_lo(x[i]);
+                            tmem_st16(t_hi + c * 16, x);
+                            if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
                         }
+                        if (kb + 1 == p.num_kb) mbar_arrive(&empty[s]);  // halo tile consumed
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(&tready[t]);
+                        if (tr) trace_ev(p, TR_S_DONE, kglob);
+                        if (++t == TSLOTS) { t = 0; tph ^= 1; }
+                        continue;
+                    }
+                    float x[32], lo[32];
+#pragma unroll
+                    for (int tp = 0; tp < 8; ++tp) {
+                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (live && tp < p.S) v = lds128(sa + kb * row_step + tp * 16);
+                        x[4 * tp] = v.x; x[4 * tp + 1] = v.y; x[4 * tp + 2] = v.z; x[4 * tp + 3] = v.w;
                     }
                     if (kb + 1 == p.num_kb) mbar_arrive(&empty[s]);  // halo tile consumed
 #pragma unroll
@@ -982,14 +1028,14 @@ __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__res
 }
 
 // Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[plane][kchunk][k][4]
-// (no-swizzle K-major core matrices, 4 reduction values per 16-byte chunk, 8
-// chunks per k-block).  Unpacked: chunk = r*8 + tap, value = channel (taps >= S
-// and channels >= C_real zero).  Packed (C=3, 7x7): value j of chunk kc is
-// reduction index q = 4kc + j = (r*S + s)*C + c, zero for q >= R*S*C.
+// (no-swizzle K-major core matrices, 4 reduction values per 16-byte chunk).
+// Unpacked: chunk = r*8 + tap, value = channel (taps >= S and channels >= C_real
+// zero).  Packed (C=3, 7x7): value j of chunk kc is reduction index
+// q = 4kc + j = (r*S + s)*C + c, zero for q >= R*S*C.
 __global__ void prepack_stem_weights_kernel(const float *__restrict__ w, float *__restrict__ out,
-                                            int K, int R, int S, int split, int C_real, int nkb,
+                                            int K, int R, int S, int split, int C_real, int nchunks,
                                             int packed) {
-    const long long plane = (long long)nkb * 8 * K * 4;
+    const long long plane = (long long)nchunks * K * 4;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
          i += (long long)gridDim.x * blockDim.x) {
         const int j = i & 3;

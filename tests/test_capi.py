@@ -43,9 +43,11 @@ def test_workspace_and_packed_bytes():
     # 3xTF32 carries the hi and lo planes
     assert L.pdl_conv2d_packed_bytes(64, 128, 3, 3, _lib.PDL_MODE_3XTF32) == 2 * 64 * 128 * 9 * 4
     assert L.pdl_conv2d_packed_bytes(64, 128, 3, 3, _lib.PDL_MODE_TF32) == 64 * 128 * 9 * 4
-    # narrow-channel stem: one k-block (8 taps x 4 channels) per kernel row
-    assert L.pdl_conv2d_packed_bytes(3, 64, 7, 7, _lib.PDL_MODE_3XTF32) == 2 * 7 * 8 * 64 * 4 * 4
+    # ResNet stem (C=3, 7x7): (r, s, c) packed, 2 k-blocks x 20 chunks of 4 values
+    assert L.pdl_conv2d_packed_bytes(3, 64, 7, 7, _lib.PDL_MODE_3XTF32) == 2 * 2 * 20 * 64 * 4 * 4
+    # other narrow shapes: one k-block (8 taps x 4 channels) per kernel row
     assert L.pdl_conv2d_packed_bytes(4, 64, 7, 7, _lib.PDL_MODE_TF32) == 7 * 8 * 64 * 4 * 4
+    assert L.pdl_conv2d_packed_bytes(3, 64, 5, 5, _lib.PDL_MODE_3XTF32) == 2 * 5 * 8 * 64 * 4 * 4
     dims = (ctypes.c_int * 10)(2, 64, 128, 14, 14, 3, 3, 1, 1, 0)
     assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 64 * 128 * 9 * 4
 
