@@ -33,7 +33,9 @@ def test_abi_version_and_cfg():
     L = _lib.lib()
     assert L.pdl_abi_version() == 1
     cfg = _lib.default_cfg(_lib.PDL_OP_CONV2D, [28, 64, 64, 56, 56, 3, 3, 1, 1, 0])
-    assert cfg.bm == 128 and cfg.bn == 64 and cfg.bk in (16, 32)
+    assert cfg.bm == 128 and cfg.bn == 64 and cfg.bk == 64   # BN=64 3x3: 64-channel k-blocks
+    cfg = _lib.default_cfg(_lib.PDL_OP_CONV2D, [28, 64, 256, 56, 56, 1, 1, 1, 0, 0])
+    assert cfg.bn == 128 and cfg.bk == 32
     cfg = _lib.default_cfg(_lib.PDL_OP_GEMM, [4096, 4096, 4096])
     assert cfg.bn in (64, 128, 256)
 

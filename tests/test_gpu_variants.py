@@ -15,7 +15,11 @@ def test_all_variants_legal(idx, mode):
     L = LAYERS[idx]
     vs = variants.generate_variants(L, variants.VariantConfig(modes=(mode,)))
     assert vs
-    dflt_bk = 32 if ((L.C + 15) // 16) % 2 == 0 else 16
+    from paper_2006_02230_b200 import _lib
+    dflt_bk = _lib.default_cfg(_lib.PDL_OP_CONV2D,
+                               [2, L.C, L.K, L.H, L.W, L.R, L.S, L.stride, L.pad, 0]).bk
+    if L.C <= 4:
+        dflt_bk = 32  # the stem ignores bk
     bad = []
     for v in vs:
         ok, d = variants.legality_check(L, v, n_images=2, seed=idx, return_detail=True)
