@@ -56,7 +56,7 @@ typedef struct pdl_tile_cfg {
     int bk;        /* reduction elements per pipeline stage (16*cg for conv)    */
     int stages;    /* smem pipeline depth                                       */
     int cluster_m; /* CTAs per cluster sharing (TMA-multicasting) a weight tile: 1|2|4 */
-    int cluster_n; /* reserved (1)                                              */
+    int cluster_n; /* 2: CTA-pair tiles, cta_group::2 MMAs with M = 256 (3xTF32 conv) */
     int split_k;   /* reserved (1)                                              */
     int raster;    /* 0: M-tiles fastest, 1: N-tiles fastest                    */
 } pdl_tile_cfg;

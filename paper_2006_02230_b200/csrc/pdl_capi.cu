@@ -101,10 +101,10 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // Persistent launch: grid = as many CTAs (clusters of CL) as can be co-resident,
 // capped by the work.  Clusters of 4 cannot use every SM (GPC granularity), so
 // the co-resident count comes from cudaOccupancyMaxActiveClusters.
-template <int KIND, int BN, int CG, bool SPLIT3, int CL>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false>
 int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_ctas, cudaStream_t s) {
-    using L = pdl::Smem<KIND, BN, CG, SPLIT3>;
-    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL>;
+    using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR>;
+    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_ctas = 0;
@@ -162,6 +162,15 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, CL>(maps, p, work, s);
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
+}
+
+// CTA-pair (cta_group::2) conv instances: 3xTF32, cluster of 2
+int dispatch_pair(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, cudaStream_t s) {
+    const int work = ((p.m_tiles + 1) / 2) * 2 * p.n_tiles;
+    if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, true, 2, true>(maps, p, work, s);
+    if (bn == 64 && cg == 2) return launch_tile<pdl::KIND_CONV, 64, 2, true, 2, true>(maps, p, work, s);
+    if (bn == 64 && cg == 4) return launch_tile<pdl::KIND_CONV, 64, 4, true, 2, true>(maps, p, work, s);
+    return fail(PDL_EUNSUPPORTED, "no CTA-pair instance for bn=%d cg=%d", bn, cg);
 }
 
 template <int KIND, bool SPLIT3>
@@ -360,8 +369,13 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         if (cfg_in->bn) cfg.bn = cfg_in->bn;
         if (cfg_in->bk) cfg.bk = cfg_in->bk;
         if (cfg_in->cluster_m) cfg.cluster_m = cfg_in->cluster_m;
+        if (cfg_in->cluster_n) cfg.cluster_n = cfg_in->cluster_n;
         cfg.raster = cfg_in->raster;
     }
+    // cluster_n == 2: the tile is computed by a CTA pair with cta_group::2 MMAs
+    // (M = 256, each CTA holds half of B); 3xTF32 only
+    const bool pair = cfg.cluster_n == 2 && split;
+    if (pair) cfg.cluster_m = 2;
     const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16, cl = cfg.cluster_m;
     const int G = weight_group(C);
     if ((G == 32) != (cg >= 2)) return fail(PDL_EINVAL, "conv: bk=%d incompatible with C=%d", cfg.bk, C);
@@ -402,8 +416,10 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         const cuuint64_t str[4] = {rowb, (cuuint64_t)K * rowb, (cuuint64_t)R * S * K * rowb,
                                    (cuuint64_t)(CT * 16 / G) * R * S * K * rowb};
         // cluster: each CTA multicasts a BN/cl-row slice of one (plane, nb) sub-tile per op
-        const cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(cfg.bn / cl), 1,
-                                    (cuuint32_t)(cl == 1 ? NB : 1), (cuuint32_t)(cl == 1 ? planes : 1)};
+        // pair: each CTA loads its BN/2 rows of every (plane, nb) sub-tile itself
+        const bool whole = cl == 1 || pair;
+        const cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(pair ? cfg.bn / 2 : cfg.bn / cl), 1,
+                                    (cuuint32_t)(whole ? NB : 1), (cuuint32_t)(whole ? planes : 1)};
         if ((rc = encode(&maps.b, wp, 5, dims, str, bbox,
                          G == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
             return rc;
@@ -433,6 +449,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
     p.raster = cfg.raster;
     p.n_tiles = (K + cfg.bn - 1) / cfg.bn;
+    if (pair) return dispatch_pair(cfg.bn, cg, maps, p, st);
     if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, cl, maps, p, st);
     return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, cl, maps, p, st);
 }

@@ -110,7 +110,9 @@ constexpr int kStemHaloBytes = 16384;  // stem halo tile: box_w * box_h * 16 B
 //           80 per tile (one TMEM slot each): 29% fewer MMAs and 5 MMA-warp passes -> 2
 constexpr int kStemPackedCG = 5;
 
-template <int KIND, int BN, int CG>
+// PAIR: the tile is computed by a CTA pair with cta_group::2 MMAs (M = 256): each
+// CTA stages its own 128 A rows and holds BN/2 rows of B.
+template <int KIND, int BN, int CG, bool PAIR = false>
 struct Geo {
     static constexpr int BM = 128;
     // stem: one stage = the whole input halo of a tile, 4 channels (16 B) per pixel
@@ -119,7 +121,7 @@ struct Geo {
     // SW64 rows make every tensor-core B read 2-way bank conflicted
     static constexpr int B_ROW = (KIND == KIND_CONV && CG == 1) ? 64 : 128;
     static constexpr int NB = KIND == KIND_CONV ? (CG >= 2 ? CG / 2 : 1) : 1;
-    static constexpr int B_SUB = KIND == KIND_STEM ? BN * 128 : BN * B_ROW;
+    static constexpr int B_SUB = KIND == KIND_STEM ? BN * 128 : (PAIR ? BN / 2 : BN) * B_ROW;
     static constexpr int NSUB = KIND == KIND_CONV ? CG : 1;
     static constexpr int A_BYTES = A_SUB * NSUB;
     static constexpr int B_BYTES = B_SUB * NB;
@@ -146,9 +148,9 @@ struct StemW {
 
 // TS = A operand staged in TMEM by the split warps (3xTF32, and the stem's tap gather).
 // SMEM stages (TMA ring) and TMEM A slots (split -> MMA ring) are separate rings.
-template <int KIND, int BN, int CG, bool SPLIT3>
+template <int KIND, int BN, int CG, bool SPLIT3, bool PAIR = false>
 struct Smem {
-    using G = Geo<KIND, BN, CG>;
+    using G = Geo<KIND, BN, CG, PAIR>;
     static constexpr bool TS = SPLIT3 || KIND == KIND_STEM;
     static constexpr int PLANES = SPLIT3 ? 2 : 1;  // B planes resident in a stage (hi, lo)
     // B planes loaded by TMA: conv / stem weights carry both (prepacked once); the
@@ -339,12 +341,13 @@ __device__ __forceinline__ void stem_gather16_kb(int c, uint32_t sa, uint32_t ro
     }
 }
 
-template <int KIND, int BN, int CG, bool SPLIT3, int CL>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
     static_assert(CL == 1 || KIND != KIND_STEM, "the stem keeps its weights resident");
-    using G = Geo<KIND, BN, CG>;
-    using L = Smem<KIND, BN, CG, SPLIT3>;
+    static_assert(!PAIR || (CL == 2 && KIND == KIND_CONV && SPLIT3), "pairs: 3xTF32 conv, cluster 2");
+    using G = Geo<KIND, BN, CG, PAIR>;
+    using L = Smem<KIND, BN, CG, SPLIT3, PAIR>;
     constexpr bool TS = L::TS;
     constexpr int STAGES = L::STAGES;
     constexpr int TSLOTS = L::TSLOTS;
@@ -388,23 +391,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // stem: only the staging warps read a stage; conv/GEMM: staging (A) + the MMA
         // commits of all CL CTAs (B is multicast into every CTA of the cluster)
-        const uint32_t empty_count = KIND == KIND_STEM ? 128 : (TS ? 128 : 0) + CL;
+        // pairs: the leader's one multicast commit per k-block reaches both CTAs;
+        // tready / tmem_empty of the leader count both CTAs' staging / epilogue
+        const uint32_t empty_count = KIND == KIND_STEM ? 128 : PAIR ? 129 : (TS ? 128 : 0) + CL;
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], empty_count);
         }
         for (int t = 0; t < TSLOTS; ++t) {
-            mbar_init(&tready[t], 128);
+            mbar_init(&tready[t], PAIR ? 256 : 128);
             mbar_init(&tfree[t], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full[b], 1);
-            mbar_init(&tmem_empty[b], kEpiThreads);
+            mbar_init(&tmem_empty[b], PAIR ? 2 * kEpiThreads : kEpiThreads);
         }
         mbar_init(wfull, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+    if (warp == 2) {
+        if constexpr (PAIR) tmem_alloc2<L::TMEM_COLS>(tmem_slot);
+        else tmem_alloc<L::TMEM_COLS>(tmem_slot);
+    }
     tc_fence_before();
     if (CL > 1) cluster_sync();  // peers multicast into our barriers: they must exist
     else __syncthreads();
@@ -481,8 +489,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tma_load_5d(sp + L::A_OFF + c * G::A_SUB, &maps.a[mi], &full[s], 0,
                                             tc.q0 + dw, tc.p0 + dh, ctg * CG + c, tc.i0);
                         }
-                        if (CL == 1) {
-                            tma_load_5d(sp + L::B_HI, &maps.b, &full[s], 0, tc.n0, rs, ctg * G::NB, 0);
+                        if (CL == 1 || PAIR) {
+                            // pair: this CTA's BN/2 rows of B (the MMA reads both halves)
+                            tma_load_5d(sp + L::B_HI, &maps.b, &full[s], 0, tc.n0 + (PAIR ? rank * (BN / 2) : 0),
+                                        rs, ctg * G::NB, 0);
                         } else {
                             // this CTA's slice: rows [rank*BN/CL, +BN/CL) of every (plane, nb) sub-tile
                             constexpr int SL = BN / CL;
@@ -503,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ===================== MMA issuer (whole warp, one elected lane issues) ============
         {
-            constexpr uint32_t idesc = idesc_tf32(128, BN, KIND == KIND_GEMM ? 1 : 0);
+            constexpr uint32_t idesc = idesc_tf32(PAIR ? 256 : 128, BN, KIND == KIND_GEMM ? 1 : 0);
             if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
                 mbar_wait(wfull, 0);
                 tc_fence_after();
@@ -512,17 +522,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0, tph = 0;
             int g = 0, kglob = 0;
             const int num_kb = p.num_kb;
-            for (int st_i = cid; st_i < num_super; st_i += ncl) {
+            // pairs: only the leader CTA issues (its MMAs drive both CTAs' tensor cores)
+            for (int st_i = cid; st_i < num_super && (!PAIR || rank == 0); st_i += ncl) {
                 int in_seg = 0;
                 uint32_t d_tmem = tmem_base;
                 for (int kb = 0; kb < num_kb; ++kb, ++kglob) {
                     if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
-                        mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
+                        if (PAIR) mbar_wait_cluster(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
+                        else mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
                         tc_fence_after();
                         d_tmem = tmem_base + (uint32_t)((g & 1) * BN);
                     }
                     if (lane == 0) trace_ev(p, TR_M_LOOP, kglob);
-                    if (TS) mbar_wait(&tready[t], tph);
+                    if (PAIR) mbar_wait_cluster(&tready[t], tph);
+                    else if (TS) mbar_wait(&tready[t], tph);
                     else mbar_wait(&full[s], ph);
                     if (lane == 0) trace_ev(p, TR_M_WAITED, kglob);
                     tc_fence_after();
@@ -550,6 +563,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             blo = smem_desc(w + StemW<BN, CG>::PLANE_BYTES, BN * 16, 128, 0);
                         }
                         if (p.flags & DBG_NO_MMA) {
+                        } else if constexpr (PAIR) {
+                            mma_ts_block2<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
+                                          G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
+                                d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
                         } else if constexpr (G::NK == 10) {  // packed stem: 8 + 2 k-steps
                             mma_ts_block<8, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2), G::boff(3),
                                          G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
@@ -586,7 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     // release the stage (B, and SS-mode A; in every CTA of the cluster)
                     // and the TMEM A slot
-                    if (KIND != KIND_STEM && TS && CL == 1) {
+                    if constexpr (PAIR) {
+                        mma_commit_pair_elect(&empty[s]);
+                        mma_commit_pair_elect(&tfree[t]);
+                    } else if (KIND != KIND_STEM && TS && CL == 1) {
                         mma_commit2_elect(&empty[s], &tfree[t]);
                     } else {
                         if (KIND != KIND_STEM) {
@@ -599,7 +619,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if (++t == TSLOTS) { t = 0; tph ^= 1; }
                     if (++in_seg == seg_kb || kb + 1 == num_kb) {
-                        mma_commit_elect(&tmem_full[g & 1]);
+                        if constexpr (PAIR) mma_commit_pair_elect(&tmem_full[g & 1]);
+                        else mma_commit_elect(&tmem_full[g & 1]);
                         in_seg = 0;
                         ++g;
                     }
@@ -746,7 +767,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tmem_wait_st();
                     tc_fence_before();
-                    mbar_arrive(&tready[t]);
+                    if (PAIR) mbar_arrive_on(&tready[t], 0);  // the leader issues for both CTAs
+                    else mbar_arrive(&tready[t]);
                     if (tr) trace_ev(p, TR_S_DONE, kglob);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if (++t == TSLOTS) { t = 0; tph ^= 1; }
@@ -788,7 +810,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&tmem_empty[g & 1]);
+                if (PAIR) mbar_arrive_on(&tmem_empty[g & 1], 0);
+                else mbar_arrive(&tmem_empty[g & 1]);
                 if (tr) trace_ev(p, TR_E_DRAINED, g);
             }
             if constexpr (KIND != KIND_GEMM) {
@@ -876,7 +899,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<L::TMEM_COLS>(tmem_base);
+        if constexpr (PAIR) tmem_dealloc2<L::TMEM_COLS>(tmem_base);
+        else tmem_dealloc<L::TMEM_COLS>(tmem_base);
     }
 }
 

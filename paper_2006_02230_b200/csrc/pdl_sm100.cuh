@@ -330,6 +330,126 @@ __device__ __forceinline__ void mma_ts_block(uint32_t d, uint32_t a, uint64_t bh
 #undef PDL_LO
 }
 
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+// The same k-block issue for an M=256 MMA spread over a CTA pair: the leader
+// issues, A comes from both CTAs' TMEM (128 rows each), B from both CTAs' smem
+// (BN/2 rows each), D lands in both CTAs' TMEM.
+#define PDL_TS_STEP2(J, OFF, SPLIT, FIRSTPRED)                                          \
+    "add.u32 ah, %1, " #J "*8;\n\t"                                                     \
+    "add.u64 bh, %2, " OFF ";\n\t"                                                      \
+    "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bh, %4, " FIRSTPRED ";\n\t"     \
+    SPLIT
+#define PDL_TS_LO2(OFF)                                                                 \
+    "add.u32 al, ah, %6;\n\t"                                                           \
+    "add.u64 bl, %3, " OFF ";\n\t"                                                      \
+    "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %4, t;\n\t"                 \
+    "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bh, %4, t;\n\t"
+
+template <int NK, bool SPLIT3, uint32_t KS, uint32_t O0, uint32_t O1, uint32_t O2, uint32_t O3,
+          uint32_t O4 = 0, uint32_t O5 = 0, uint32_t O6 = 0, uint32_t O7 = 0>
+__device__ __forceinline__ void mma_ts_block2(uint32_t d, uint32_t a, uint64_t bhi, uint64_t blo,
+                                             uint32_t idesc, uint32_t acc) {
+    static_assert(NK == 2 || NK == 4 || NK == 8, "k-steps per block");
+#define PDL_LO2(OFF) (SPLIT3 ? PDL_TS_LO2(OFF) : "")
+    if constexpr (NK == 2) {
+        if constexpr (SPLIT3)
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP2(0, "%7", PDL_TS_LO2("%7"), "p") PDL_TS_STEP2(1, "%8", PDL_TS_LO2("%8"), "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP2(0, "%7", "", "p") PDL_TS_STEP2(1, "%8", "", "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1) : "memory");
+    } else if constexpr (NK == 4) {
+        if constexpr (SPLIT3)
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP2(0, "%7", PDL_TS_LO2("%7"), "p") PDL_TS_STEP2(1, "%8", PDL_TS_LO2("%8"), "t")
+                         PDL_TS_STEP2(2, "%9", PDL_TS_LO2("%9"), "t") PDL_TS_STEP2(3, "%10", PDL_TS_LO2("%10"), "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3) : "memory");
+        else
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP2(0, "%7", "", "p") PDL_TS_STEP2(1, "%8", "", "t")
+                         PDL_TS_STEP2(2, "%9", "", "t") PDL_TS_STEP2(3, "%10", "", "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3) : "memory");
+    } else {
+        if constexpr (SPLIT3)
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP2(0, "%7", PDL_TS_LO2("%7"), "p") PDL_TS_STEP2(1, "%8", PDL_TS_LO2("%8"), "t")
+                         PDL_TS_STEP2(2, "%9", PDL_TS_LO2("%9"), "t") PDL_TS_STEP2(3, "%10", PDL_TS_LO2("%10"), "t")
+                         PDL_TS_STEP2(4, "%11", PDL_TS_LO2("%11"), "t") PDL_TS_STEP2(5, "%12", PDL_TS_LO2("%12"), "t")
+                         PDL_TS_STEP2(6, "%13", PDL_TS_LO2("%13"), "t") PDL_TS_STEP2(7, "%14", PDL_TS_LO2("%14"), "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3), "n"(O4), "n"(O5), "n"(O6), "n"(O7)
+                         : "memory");
+        else
+            asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+                         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                         PDL_TS_STEP2(0, "%7", "", "p") PDL_TS_STEP2(1, "%8", "", "t")
+                         PDL_TS_STEP2(2, "%9", "", "t") PDL_TS_STEP2(3, "%10", "", "t")
+                         PDL_TS_STEP2(4, "%11", "", "t") PDL_TS_STEP2(5, "%12", "", "t")
+                         PDL_TS_STEP2(6, "%13", "", "t") PDL_TS_STEP2(7, "%14", "", "t")
+                         "}" ::"r"(d), "r"(a), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc), "n"(KS),
+                         "n"(O0), "n"(O1), "n"(O2), "n"(O3), "n"(O4), "n"(O5), "n"(O6), "n"(O7)
+                         : "memory");
+    }
+#undef PDL_LO2
+}
+
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_alloc2(uint32_t *slot_smem) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(slot_smem)),
+                 "n"(NCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS)
+                 : "memory");
+}
+// Leader-issued commit that arrives on the barrier at the same smem offset in
+// both CTAs of the pair once the pair's MMAs complete.
+__device__ __forceinline__ void mma_commit_pair_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// Arrive (release, cluster scope) on the barrier at the same smem offset in CTA `cta`.
+__device__ __forceinline__ void mbar_arrive_on(uint64_t *bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+// Wait with cluster-scope acquire (the barrier receives remote arrivals).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Two commits (stage release, A-slot release) from one elected lane.
 __device__ __forceinline__ void mma_commit2_elect(uint64_t *bar0, uint64_t *bar1) {
     asm volatile(

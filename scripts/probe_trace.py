@@ -12,6 +12,8 @@ out = {}
 import os
 CL = int(os.environ.get("CL", "0"))
 cfg = {"cluster_m": CL} if CL else None
+if os.environ.get("PAIR"):
+    cfg = {"cluster_n": 2}
 class _G:
     def __init__(self, m): self.m = m
     def name(self): return f"gemm{self.m}"

@@ -26,3 +26,19 @@ def test_all_variants_legal(idx, mode):
         if not ok or (v.bk == dflt_bk and not d["bitwise"]):
             bad.append((v.vid, d))
     assert not bad, bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", [3, 7, 19])
+def test_cta_pair_tiles_bitwise_equal(idx):
+    """cluster_n=2: cta_group::2 MMAs over a CTA pair (M=256, B split across the
+    pair) give bitwise the single-CTA result (same per-element reduction order)."""
+    import torch
+    import paper_2006_02230_b200 as P
+    from paper_2006_02230_b200.workloads import conv_inputs
+    L = LAYERS[idx]
+    x, w, b = (torch.from_numpy(t).cuda() for t in conv_inputs(L, 3, seed=idx))
+    pw = P.prepack_weights(w, channels=L.C)
+    ref = P.conv2d_nchw16c(x, pw, b, stride=L.stride, pad=L.pad, relu=True)
+    got = P.conv2d_nchw16c(x, pw, b, stride=L.stride, pad=L.pad, relu=True, cfg={"cluster_n": 2})
+    assert torch.equal(ref, got)
