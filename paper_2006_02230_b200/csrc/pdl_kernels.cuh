@@ -103,7 +103,10 @@ struct TmaMaps {
 //   CONV: A [CG][128 rows][16]    SW64  K-major        B [CG/2][BN rows][32] SW128 K-major
 //                                                      (CG = 1: B [BN rows][16] SW64)
 //   STEM: A halo tile [rows][px][4 fp32], no swizzle   B resident: [plane][chunk][BN][4]
-constexpr int kStemHaloBytes = 16384;  // stem halo tile: box_w * box_h * 16 B
+constexpr int kStemHaloBytes = 16384;
+#ifndef PDL_EPI_BUFS
+#define PDL_EPI_BUFS 2
+#endif  // stem halo tile: box_w * box_h * 16 B
 // For KIND_STEM the CG template parameter selects the reduction packing:
 //   CG = 1: k-block = one kernel row, K = 8 taps x 4 channels = 32 (any C <= 4, S <= 8)
 //   CG = kStemPackedCG: K = (r, s, c) dense for C = 3, 7x7 (147 -> 160), two k-blocks of
@@ -163,8 +166,12 @@ struct Smem {
     static constexpr int STAGE = KIND == KIND_STEM ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
     // conv / stem epilogue: one 128-row x 16-channel (8 KB, SW64) TMA-store buffer
     // per column half of the epilogue warps
-    static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * 8192;
-    static constexpr int BUDGET = 216 * 1024 - W_BYTES - EPI_BYTES;
+    // two output-box buffers per column half: a box is filled while the previous
+    // one drains (one buffer serialised the epilogue on each TMA store's smem read)
+    static constexpr int EPI_BUFS = PDL_EPI_BUFS;
+    static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * EPI_BUFS * 8192;
+    // 227 KB opt-in dynamic smem per CTA, minus 2 KB for barriers + base alignment
+    static constexpr int BUDGET = 232448 - 2048 - W_BYTES - EPI_BYTES;
     static constexpr int S0 = BUDGET / STAGE;
     static constexpr int STAGES = S0 > 16 ? 16 : S0;
     static constexpr int SLOT_COLS = SPLIT3 ? 2 * G::KS : G::KS;  // TMEM columns per A slot
@@ -178,6 +185,7 @@ struct Smem {
     static constexpr int EPI_OFF = W_OFF + W_BYTES;
     static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
     static constexpr int TOTAL = BAR_OFF + 1024 + 1024;  // barriers + alignment slack
+    static_assert(TOTAL <= 232448, "shared memory over the 227 KB per-CTA limit");
     static constexpr uint32_t TMEM_COLS = TS ? 512 : 2 * BN;
     static_assert(STAGES >= 2, "tile too large for a 2-stage pipeline");
     static_assert(!TS || TSLOTS >= 2, "not enough TMEM for two A slots");
@@ -785,6 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
         const bool tr = e == 0 && lane == 0;
         int g = 0, jt = 0;
+        uint32_t eblk = 0;  // output boxes issued by this half (epilogue buffer ring)
         for (int st_i = cid; st_i < num_super; st_i += ncl, ++jt) {
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
             float sum[HALF];
@@ -818,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // ---- store via TMA (bias + ReLU fused): per 16-channel block, the half's
                 // 128 threads write their pixel's 64 bytes into a SW64 smem image of the
                 // output box, one thread stores the box; TMA clips pixels outside P x Q
-                const uint32_t ebuf = smem0 + L::EPI_OFF + half * 8192;
+                const uint32_t ebase = smem0 + L::EPI_OFF + half * L::EPI_BUFS * 8192;
                 const bool in_box = row < p.BW * p.BH * p.BNI;
                 const bool leader = quarter == 0 && lane == 0;
                 const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
@@ -826,7 +835,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < HALF / 16; ++j) {
                     const int col0 = tc.n0 + half * HALF + j * 16;
-                    if (leader) bulk_wait_read<0>();  // previous box left the buffer
+                    const uint32_t ebuf = ebase + (uint32_t)(eblk % L::EPI_BUFS) * 8192;
+                    ++eblk;
+                    if (leader) bulk_wait_read<L::EPI_BUFS - 1>();  // this buffer's last box left
                     named_bar_sync(2 + half, 128);
                     if (in_box) {
 #pragma unroll
@@ -848,9 +859,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     fence_proxy_async_smem();
                     named_bar_sync(2 + half, 128);
-                    if (leader && col0 < p.n_out && !(p.flags & DBG_NO_EPI_STORE)) {
-                        tma_store_5d(&maps.y, ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
-                        bulk_commit();
+                    if (leader) {
+                        if (col0 < p.n_out && !(p.flags & DBG_NO_EPI_STORE))
+                            tma_store_5d(&maps.y, ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
+                        bulk_commit();  // one group per block (possibly empty): uniform ring
                     }
                 }
                 if (tr) trace_ev(p, TR_E_STORED, jt);
