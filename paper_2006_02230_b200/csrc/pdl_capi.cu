@@ -101,10 +101,10 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // Persistent launch: grid = as many CTAs (clusters of CL) as can be co-resident,
 // capped by the work.  Clusters of 4 cannot use every SM (GPC granularity), so
 // the co-resident count comes from cudaOccupancyMaxActiveClusters.
-template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0>
 int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_ctas, cudaStream_t s) {
-    using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR>;
-    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR>;
+    using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR, RESW>;
+    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR, RESW>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_ctas = 0;
@@ -132,7 +132,7 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
     if (attr_err != cudaSuccess)
         return fail(PDL_ELAUNCH, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
     int grid = std::min(max_ctas, (work_ctas + CL - 1) / CL * CL);
-    if (KIND == pdl::KIND_STEM) grid = std::max(p.n_tiles, grid / p.n_tiles * p.n_tiles);
+    if (KIND == pdl::KIND_STEM || RESW) grid = std::max(p.n_tiles, grid / p.n_tiles * p.n_tiles);
     lc.gridDim = dim3(grid);
     pdl::TileParams pt = p;
     pt.trace = g_trace;
@@ -162,6 +162,21 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, CL>(maps, p, work, s);
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
+}
+
+// Resident-weight 1x1 conv instances (3xTF32, cluster 1): RESW bytes per plane
+int dispatch_resident(int bn, int cg, int plane_bytes, const pdl::TmaMaps &maps,
+                      const pdl::TileParams &p, cudaStream_t s) {
+    const int work = p.m_tiles * p.n_tiles;
+    if (cg == 2 && plane_bytes <= 32768) {
+        if (bn == 128) return launch_tile<pdl::KIND_CONV, 128, 2, true, 1, false, 32768>(maps, p, work, s);
+        if (bn == 64) return launch_tile<pdl::KIND_CONV, 64, 2, true, 1, false, 32768>(maps, p, work, s);
+    }
+    if (cg == 2 && plane_bytes <= 65536) {
+        if (bn == 128) return launch_tile<pdl::KIND_CONV, 128, 2, true, 1, false, 65536>(maps, p, work, s);
+        if (bn == 64) return launch_tile<pdl::KIND_CONV, 64, 2, true, 1, false, 65536>(maps, p, work, s);
+    }
+    return fail(PDL_EUNSUPPORTED, "no resident-weight instance for bn=%d cg=%d (%d B)", bn, cg, plane_bytes);
 }
 
 // CTA-pair (cta_group::2) conv instances: 3xTF32, cluster of 2
@@ -376,6 +391,12 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // (M = 256, each CTA holds half of B); 3xTF32 only
     const bool pair = cfg.cluster_n == 2 && split;
     if (pair) cfg.cluster_m = 2;
+    // 1x1 convs whose N-tile weight slice fits in 64 KB per plane keep it resident
+    // (loaded once per CTA; stages carry A only) unless a multicast cluster is asked for
+    const int res_plane = ceil16(C) * 16 * cfg.bn * 4;
+    const bool resident = split && !pair && R == 1 && S == 1 && cfg.bk == 32 && res_plane <= 65536 &&
+                          (!cfg_in || cfg_in->cluster_m <= 1);
+    if (resident) cfg.cluster_m = 1;
     const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16, cl = cfg.cluster_m;
     const int G = weight_group(C);
     if ((G == 32) != (cg >= 2)) return fail(PDL_EINVAL, "conv: bk=%d incompatible with C=%d", cfg.bk, C);
@@ -416,10 +437,16 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         const cuuint64_t str[4] = {rowb, (cuuint64_t)K * rowb, (cuuint64_t)R * S * K * rowb,
                                    (cuuint64_t)(CT * 16 / G) * R * S * K * rowb};
         // cluster: each CTA multicasts a BN/cl-row slice of one (plane, nb) sub-tile per op
-        // pair: each CTA loads its BN/2 rows of every (plane, nb) sub-tile itself
+        // pair: each CTA loads its BN/2 rows of every (plane, nb) sub-tile itself;
+        // resident: one box = the N-tile's whole slice of one plane
         const bool whole = cl == 1 || pair;
-        const cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(pair ? cfg.bn / 2 : cfg.bn / cl), 1,
-                                    (cuuint32_t)(whole ? NB : 1), (cuuint32_t)(whole ? planes : 1)};
+        cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(pair ? cfg.bn / 2 : cfg.bn / cl), 1,
+                              (cuuint32_t)(whole ? NB : 1), (cuuint32_t)(whole ? planes : 1)};
+        if (resident) {
+            bbox[1] = (cuuint32_t)cfg.bn;
+            bbox[3] = (cuuint32_t)(CT * 16 / G);
+            bbox[4] = 1;
+        }
         if ((rc = encode(&maps.b, wp, 5, dims, str, bbox,
                          G == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
             return rc;
@@ -450,6 +477,10 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.raster = cfg.raster;
     p.n_tiles = (K + cfg.bn - 1) / cfg.bn;
     if (pair) return dispatch_pair(cfg.bn, cg, maps, p, st);
+    if (resident) {
+        p.res_bytes = res_plane;
+        return dispatch_resident(cfg.bn, cg, res_plane, maps, p, st);
+    }
     if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, cl, maps, p, st);
     return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, cl, maps, p, st);
 }

@@ -56,6 +56,7 @@ struct TileParams {
     int BW, BH, BNI;       // box of output pixels per tile
     int tiles_w, tiles_h;  // tile grid over (Q, P); images fastest-after
     int box_w, box_h;      // stem: halo tile (input pixels x input rows) of one output tile
+    int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
     int raster;            // reserved
@@ -151,7 +152,9 @@ struct StemW {
 
 // TS = A operand staged in TMEM by the split warps (3xTF32, and the stem's tap gather).
 // SMEM stages (TMA ring) and TMEM A slots (split -> MMA ring) are separate rings.
-template <int KIND, int BN, int CG, bool SPLIT3, bool PAIR = false>
+// RESW (1x1 conv): the N-tile's whole weight slice stays resident in smem (RESW
+// bytes reserved per plane), loaded once per CTA; stages then carry A only.
+template <int KIND, int BN, int CG, bool SPLIT3, bool PAIR = false, int RESW = 0>
 struct Smem {
     using G = Geo<KIND, BN, CG, PAIR>;
     static constexpr bool TS = SPLIT3 || KIND == KIND_STEM;
@@ -162,8 +165,8 @@ struct Smem {
     // staging warps' smem traffic costs more than the TMA bytes it saves.)
     static constexpr int LOAD_PLANES = KIND == KIND_GEMM ? 1 : PLANES;
     // stem weights stay resident for the whole kernel (one N-tile per CTA)
-    static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * StemW<BN, CG>::PLANE_BYTES : 0;
-    static constexpr int STAGE = KIND == KIND_STEM ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
+    static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * StemW<BN, CG>::PLANE_BYTES : PLANES * RESW;
+    static constexpr int STAGE = (KIND == KIND_STEM || RESW) ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
     // conv / stem epilogue: one 128-row x 16-channel (8 KB, SW64) TMA-store buffer
     // per column half of the epilogue warps
     // two output-box buffers per column half: a box is filled while the previous
@@ -349,13 +352,14 @@ __device__ __forceinline__ void stem_gather16_kb(int c, uint32_t sa, uint32_t ro
     }
 }
 
-template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
     static_assert(CL == 1 || KIND != KIND_STEM, "the stem keeps its weights resident");
     static_assert(!PAIR || (CL == 2 && KIND == KIND_CONV && SPLIT3), "pairs: 3xTF32 conv, cluster 2");
+    static_assert(!RESW || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3), "resident weights: 3xTF32 conv");
     using G = Geo<KIND, BN, CG, PAIR>;
-    using L = Smem<KIND, BN, CG, SPLIT3, PAIR>;
+    using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW>;
     constexpr bool TS = L::TS;
     constexpr int STAGES = L::STAGES;
     constexpr int TSLOTS = L::TSLOTS;
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // commits of all CL CTAs (B is multicast into every CTA of the cluster)
         // pairs: the leader's one multicast commit per k-block reaches both CTAs;
         // tready / tmem_empty of the leader count both CTAs' staging / epilogue
-        const uint32_t empty_count = KIND == KIND_STEM ? 128 : PAIR ? 129 : (TS ? 128 : 0) + CL;
+        const uint32_t empty_count = (KIND == KIND_STEM || RESW) ? 128 : PAIR ? 129 : (TS ? 128 : 0) + CL;
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], empty_count);
@@ -435,8 +439,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
             else if (KIND == KIND_CONV)
                 tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
-                                G::B_BYTES * L::LOAD_PLANES);
+                                (RESW ? 0 : G::B_BYTES * L::LOAD_PLANES));
             else tx = (uint32_t)(16 * p.box_w * p.box_h);
+            if (RESW && blockIdx.x < num_tiles) {
+                // the grid is a multiple of n_tiles: this CTA keeps one N-tile throughout
+                const int n0 = (blockIdx.x % p.n_tiles) * BN;
+                mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.res_bytes));
+                for (int pl = 0; pl < L::PLANES; ++pl)
+                    tma_load_5d(smem + L::W_OFF + pl * RESW, &maps.b, wfull, 0, n0, 0, 0, pl);
+            }
             if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
                 // resident weights of this CTA's N-tile: [plane][kb][KS/4 chunks][BN][4]
                 const int n0 = (blockIdx.x % p.n_tiles) * BN;
@@ -497,7 +508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tma_load_5d(sp + L::A_OFF + c * G::A_SUB, &maps.a[mi], &full[s], 0,
                                             tc.q0 + dw, tc.p0 + dh, ctg * CG + c, tc.i0);
                         }
-                        if (CL == 1 || PAIR) {
+                        if (RESW) {
+                        } else if (CL == 1 || PAIR) {
                             // pair: this CTA's BN/2 rows of B (the MMA reads both halves)
                             tma_load_5d(sp + L::B_HI, &maps.b, &full[s], 0, tc.n0 + (PAIR ? rank * (BN / 2) : 0),
                                         rs, ctg * G::NB, 0);
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== MMA issuer (whole warp, one elected lane issues) ============
         {
             constexpr uint32_t idesc = idesc_tf32(PAIR ? 256 : 128, BN, KIND == KIND_GEMM ? 1 : 0);
-            if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
+            if ((KIND == KIND_STEM || RESW) && blockIdx.x < num_tiles) {  // CL == 1 here
                 mbar_wait(wfull, 0);
                 tc_fence_after();
             }
@@ -559,6 +571,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // chunks at LBO = 32 rows * 128B.
                             bhi = smem_desc(st + L::B_HI, 4096, 512, LAYOUT_SW128_B32);
                             blo = smem_desc(st + L::B_LO, 4096, 512, LAYOUT_SW128_B32);
+                        } else if (KIND == KIND_CONV && RESW) {
+                            // resident [plane][channel group][BN rows][G]: k-block kb = NB groups
+                            const uint32_t lay = G::B_ROW == 128 ? LAYOUT_SW128 : LAYOUT_SW64;
+                            const uint32_t w = smem0 + L::W_OFF + (uint32_t)(kb * G::B_BYTES);
+                            bhi = smem_desc(w, 16, 8 * G::B_ROW, lay);
+                            blo = smem_desc(w + RESW, 16, 8 * G::B_ROW, lay);
                         } else if (KIND == KIND_CONV) {
                             const uint32_t lay = G::B_ROW == 128 ? LAYOUT_SW128 : LAYOUT_SW64;
                             bhi = smem_desc(st + L::B_HI, 16, 8 * G::B_ROW, lay);
@@ -614,6 +632,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (PAIR) {
                         mma_commit_pair_elect(&empty[s]);
                         mma_commit_pair_elect(&tfree[t]);
+                    } else if (RESW) {
+                        mma_commit_elect(&tfree[t]);  // the stage held only A (read by staging)
                     } else if (KIND != KIND_STEM && TS && CL == 1) {
                         mma_commit2_elect(&empty[s], &tfree[t]);
                     } else {
