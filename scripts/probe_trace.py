@@ -53,6 +53,12 @@ for arg in (sys.argv[1:] or ["3", "7", "4", "17"]):
     if len(es) > 2:
         print(f"  epilogue: full->drained median {np.median(ed[:len(ef)] - ef[:len(ed)]):.0f}, tiles {len(es)}, "
               f"store spacing {np.median(np.diff(es)):.0f}")
+        nseg = max(1, len(ed) // max(1, len(es)))
+        if nseg == 1 and len(ed) >= len(es):
+            st = es[:len(ed)] - ed[:len(es)]
+            wait_next = ef[1:len(es)] - es[:len(ef) - 1]
+            print(f"  epilogue: drained->stored median {np.median(st):.0f}, stored->next full median "
+                  f"{np.median(wait_next):.0f}")
     mma_wait = int(np.sum(np.maximum(mr[1:] - mi[:-1], 0)))
     gap = np.median(mr[1:] - mi[:-1])
     ml, mw = col("M_LOOP"), col("M_WAITED")
