@@ -100,6 +100,24 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
                              int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg,
                              void *stream);
 
+/* Host-buffer convolution -- the reference's interpret() contract (host arrays
+ * in, fresh host arrays out: simcache.py:89-204, inputs copied at :110).
+ * x_host [N][C/16][H][W][16] and y_host [N][K/16][P][Q][16] are HOST pointers
+ * (pinned -- cudaHostAlloc / cudaHostRegister -- or the copies serialise);
+ * packed_w / bias / workspace are device pointers.  The minibatch is cut into
+ * chunks of `chunk` images (0 = library default, ~16 MB of x per chunk); each
+ * chunk's host->device copy, convolution (on `stream`) and device->host copy
+ * run on separate streams through 3 staging slots, so both PCIe directions and
+ * the tensor cores overlap.  Ordered after prior work on `stream`; work
+ * enqueued on `stream` after the call sees y_host complete.  workspace must
+ * hold pdl_conv2d_host_workspace_bytes(...) bytes (same chunk). */
+size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R, int S,
+                                       int stride, int pad, int chunk);
+int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *bias,
+                        float *y_host, int N, int C, int K, int H, int W, int R, int S,
+                        int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg, int chunk,
+                        void *workspace, size_t ws_bytes, void *stream);
+
 /* C = alpha * A B + beta * C, row-major with leading dimensions lda/ldb/ldc. */
 int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda,
                  int ldb, int ldc, float alpha, float beta, unsigned flags,

@@ -32,7 +32,7 @@ EXPORTS = (
     "pdl_conv2d_fwd_prepacked", "pdl_gemm_f32", "pdl_bias_relu_nchw16c",
     "pdl_workspace_bytes", "pdl_default_cfg", "pdl_last_launch_count", "pdl_last_error",
     "pdl_abi_version", "pdl_device_check", "pdl_pack_nchw16c", "pdl_unpack_nchw16c",
-    "pdl_pack_kcrs16c16k",
+    "pdl_pack_kcrs16c16k", "pdl_conv2d_host_workspace_bytes", "pdl_conv2d_fwd_host",
 )
 
 
@@ -84,6 +84,10 @@ def _declare(L):
     L.pdl_conv2d_prepack_weights.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
     L.pdl_conv2d_fwd_prepacked.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
         _u, ctypes.POINTER(TileCfg), _vp]
+    L.pdl_conv2d_host_workspace_bytes.argtypes = [_i] * 10
+    L.pdl_conv2d_host_workspace_bytes.restype = _sz
+    L.pdl_conv2d_fwd_host.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
+        _u, ctypes.POINTER(TileCfg), _i, _vp, _sz, _vp]
     L.pdl_gemm_f32.argtypes = [_vp, _vp, _vp] + [_i] * 6 + [
         ctypes.c_float, ctypes.c_float, _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
     L.pdl_bias_relu_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
@@ -99,7 +103,8 @@ def _declare(L):
     L.pdl_abi_version.argtypes = []
     L.pdl_device_check.argtypes = []
     for name in EXPORTS:
-        if name not in ("pdl_conv2d_packed_bytes", "pdl_workspace_bytes", "pdl_last_error"):
+        if name not in ("pdl_conv2d_packed_bytes", "pdl_workspace_bytes", "pdl_last_error",
+                        "pdl_conv2d_host_workspace_bytes"):
             getattr(L, name).restype = _i
 
 

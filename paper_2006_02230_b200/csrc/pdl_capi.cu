@@ -485,6 +485,48 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, cl, maps, p, st);
 }
 
+// ---------------------------------------------------------------- host-buffer pipeline
+// Per-thread, per-device copy streams and slot events of pdl_conv2d_fwd_host.
+constexpr int kHostSlots = 3;     // device staging slots (x and y) in flight
+constexpr int kMaxDevices = 16;
+struct HostPipe {
+    bool ready = false;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t entry = nullptr, x_in[kHostSlots], done[kHostSlots], y_out[kHostSlots];
+};
+thread_local HostPipe g_pipe[kMaxDevices];
+
+int host_pipe(HostPipe **out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return fail(PDL_EDEVICE, "conv host: no current device");
+    HostPipe &hp = g_pipe[dev];
+    if (!hp.ready) {
+        const unsigned ef = cudaEventDisableTiming;
+        bool ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&hp.entry, ef) == cudaSuccess;
+        for (int i = 0; ok && i < kHostSlots; ++i)
+            ok = cudaEventCreateWithFlags(&hp.x_in[i], ef) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&hp.done[i], ef) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&hp.y_out[i], ef) == cudaSuccess;
+        if (!ok) return fail(PDL_ELAUNCH, "conv host: stream/event creation failed");
+        hp.ready = true;
+    }
+    *out = &hp;
+    return PDL_OK;
+}
+
+// Images per pipeline chunk: ~16 MB of x per copy (PCIe-efficient transfers), at
+// least 4 chunks when the batch allows (so both copy directions overlap).
+int host_chunk(int N, size_t x_img) {
+    const size_t target = (size_t)16 << 20;
+    int c = (int)std::max<size_t>(1, target / std::max<size_t>(x_img, 1));
+    return std::max(1, std::min(c, (N + 3) / 4));
+}
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
 }  // namespace
 
 extern "C" {
@@ -546,6 +588,88 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
     if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
     return conv_fwd_tc(x, reinterpret_cast<const float *>(packed_w), bias, y, N, C, K, H, W, R, S,
                        stride, pad, flags, cfg, (cudaStream_t)stream);
+}
+
+size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R, int S, int stride,
+                                       int pad, int chunk) {
+    if (N <= 0 || C <= 0 || K <= 0 || H <= 0 || W <= 0 || stride <= 0) return 0;
+    const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+    if (P <= 0 || Q <= 0) return 0;
+    const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
+    const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
+    return (size_t)kHostSlots * (align256(c * x_img) + align256(c * y_img));
+}
+
+int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *bias,
+                        float *y_host, int N, int C, int K, int H, int W, int R, int S,
+                        int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg, int chunk,
+                        void *workspace, size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if (!x_host || !y_host) return fail(PDL_EINVAL, "conv host: null host buffer");
+    if (chunk < 0) return fail(PDL_EINVAL, "conv host: negative chunk");
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
+        return fail(PDL_EUNSUPPORTED, "conv host: PDL_MODE_FP32 takes raw weights (pdl_conv2d_fwd_nchw16c)");
+    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if (!aligned16(packed_w) || !aligned16(workspace))
+        return fail(PDL_EALIGN, "conv host: packed weights / workspace unaligned");
+    // shape checks before anything is enqueued (workspace stands in for x / y)
+    if ((rc = conv_check((const float *)workspace, (const float *)workspace, N, C, K, H, W, R, S,
+                         stride, pad)))
+        return rc;
+    const size_t need = pdl_conv2d_host_workspace_bytes(N, C, K, H, W, R, S, stride, pad, chunk);
+    if (!workspace || ws_bytes < need)
+        return fail(PDL_EWORKSPACE, "conv host: workspace of %zu bytes required", need);
+    HostPipe *hp;
+    if ((rc = host_pipe(&hp))) return rc;
+    const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+    const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
+    const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
+    const size_t xs = align256(c * x_img), ys = align256(c * y_img);
+    uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
+    cudaStream_t st = (cudaStream_t)stream;
+    // chunk i uses slot i % kHostSlots:
+    //   h2d: [slot's previous conv done] copy x  -> x_in
+    //   st : [x_in, slot's previous y copy done] conv -> done
+    //   d2h: [done] copy y -> y_out
+    // entry orders the first use of every slot after prior work on `stream`.
+    if (cudaEventRecord(hp->entry, st) != cudaSuccess || cudaStreamWaitEvent(hp->h2d, hp->entry, 0) != cudaSuccess)
+        return fail(PDL_ELAUNCH, "conv host: entry event");
+    const int nchunks = (N + c - 1) / c;
+    int launches = 0;
+    for (int i = 0; i < nchunks; ++i) {
+        const int b = i % kHostSlots;
+        const int n0 = i * c, n = std::min(c, N - n0);
+        float *xd = reinterpret_cast<float *>(ws + b * (xs + ys));
+        float *yd = reinterpret_cast<float *>(ws + b * (xs + ys) + xs);
+        if (i >= kHostSlots && cudaStreamWaitEvent(hp->h2d, hp->done[b], 0) != cudaSuccess)
+            return fail(PDL_ELAUNCH, "conv host: wait");
+        if (cudaMemcpyAsync(xd, reinterpret_cast<const uint8_t *>(x_host) + n0 * x_img, n * x_img,
+                            cudaMemcpyHostToDevice, hp->h2d) != cudaSuccess ||
+            cudaEventRecord(hp->x_in[b], hp->h2d) != cudaSuccess)
+            return fail(PDL_ELAUNCH, "conv host: H2D copy: %s", cudaGetErrorString(cudaGetLastError()));
+        if (cudaStreamWaitEvent(st, hp->x_in[b], 0) != cudaSuccess ||
+            (i >= kHostSlots && cudaStreamWaitEvent(st, hp->y_out[b], 0) != cudaSuccess))
+            return fail(PDL_ELAUNCH, "conv host: wait");
+        if ((rc = conv_fwd_tc(xd, reinterpret_cast<const float *>(packed_w), bias, yd, n, C, K, H, W,
+                              R, S, stride, pad, flags, cfg, st)))
+            return rc;
+        launches += g_launches;
+        if (cudaEventRecord(hp->done[b], st) != cudaSuccess ||
+            cudaStreamWaitEvent(hp->d2h, hp->done[b], 0) != cudaSuccess ||
+            cudaMemcpyAsync(reinterpret_cast<uint8_t *>(y_host) + n0 * y_img, yd, n * y_img,
+                            cudaMemcpyDeviceToHost, hp->d2h) != cudaSuccess ||
+            cudaEventRecord(hp->y_out[b], hp->d2h) != cudaSuccess)
+            return fail(PDL_ELAUNCH, "conv host: D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    // later work on `stream` (and the next call's slot reuse) sees every y copy done
+    for (int b = 0; b < std::min(nchunks, kHostSlots); ++b)
+        if (cudaStreamWaitEvent(st, hp->y_out[b], 0) != cudaSuccess)
+            return fail(PDL_ELAUNCH, "conv host: exit wait");
+    g_launches = launches;
+    return PDL_OK;
 }
 
 int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, float *y, int N,

@@ -131,6 +131,57 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
     return y
 
 
+_host_ws: dict = {}
+
+
+def _host_workspace(device, nbytes: int) -> torch.Tensor:
+    """Device staging for conv2d_nchw16c_host, kept per device and grown on demand
+    (every call joins its copy streams back into the caller's stream, so the
+    next call may reuse it)."""
+    key = torch.device(device).index
+    ws = _host_ws.get(key)
+    if ws is None or ws.numel() * 4 < nbytes:
+        ws = torch.empty((nbytes + 3) // 4, dtype=torch.float32, device=device)
+        _host_ws[key] = ws
+    return ws
+
+
+def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | None = None,
+                        stride: int = 1, pad: int = 0, relu: bool = False, mode: str = "3xtf32",
+                        cfg=None, out: torch.Tensor | None = None, chunk: int = 0,
+                        device=None, stream=None) -> torch.Tensor:
+    """Blocked conv fwd over HOST buffers (the reference's interpret() contract:
+    host arrays in, host array out).  x / out are CPU float32 tensors -- pinned
+    for full PCIe speed -- weights (PackedWeights) and bias live on the GPU.  The
+    library pipelines image chunks: H2D copy, fused conv and D2H copy overlap
+    (pdl_conv2d_fwd_host).  Returns `out` (allocated pinned if None), complete
+    once `stream` reaches the point after this call."""
+    if not isinstance(w, PackedWeights):
+        raise TypeError("conv2d_nchw16c_host takes PackedWeights (prepack_weights())")
+    if not isinstance(x, torch.Tensor) or x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+        raise TypeError("x must be a contiguous float32 CPU tensor")
+    _need_cuda_f32("bias", bias)
+    if w.mode != mode.lower():
+        raise ValueError(f"weights packed for {w.mode}, called with {mode}")
+    n, ct, h, wd, v = x.shape
+    if v != 16 or not (ct * 16 - 16 < w.C <= ct * 16):
+        raise ValueError(f"x must be nChw16c with {w.C} channels")
+    P, Q = conv_out_hw(h, wd, w.R, w.S, stride, pad)
+    y = out if out is not None else torch.empty((n, w.K // 16, P, Q, 16), dtype=torch.float32,
+                                                pin_memory=True)
+    if y.is_cuda or y.dtype != torch.float32 or not y.is_contiguous() or \
+            tuple(y.shape) != (n, w.K // 16, P, Q, 16):
+        raise ValueError("out must be a contiguous float32 CPU tensor [N][K/16][P][Q][16]")
+    dev = w.data.device if device is None else torch.device(device)
+    need = lib().pdl_conv2d_host_workspace_bytes(n, w.C, w.K, h, wd, w.R, w.S, stride, pad, chunk)
+    ws = _host_workspace(dev, need)
+    flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    check(lib().pdl_conv2d_fwd_host(_ptr(x), _ptr(w.data), _ptr(bias), _ptr(y), n, w.C, w.K, h, wd,
+                                    w.R, w.S, stride, pad, flags, _cfg_ptr(cfg), int(chunk),
+                                    _ptr(ws), ws.numel() * 4, ctypes.c_void_p(_stream(stream))))
+    return y
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha: float = 1.0,
          beta: float = 0.0, relu: bool = False, mode: str = "3xtf32", cfg=None,
          stream=None) -> torch.Tensor:
