@@ -57,7 +57,8 @@ typedef struct pdl_tile_cfg {
     int stages;    /* smem pipeline depth                                       */
     int cluster_m; /* CTAs per cluster sharing (TMA-multicasting) a weight tile: 1|2|4 */
     int cluster_n; /* 2: CTA-pair tiles, cta_group::2 MMAs with M = 256 (3xTF32 conv) */
-    int split_k;   /* reserved (1)                                              */
+    int split_k;   /* 0: auto (split the reduction when the tiles leave SMs idle
+                      and a workspace is given), 1: off, >1: that many ranges   */
     int raster;    /* 0: M-tiles fastest, 1: N-tiles fastest                    */
 } pdl_tile_cfg;
 
@@ -83,8 +84,9 @@ enum {
 enum { PDL_OP_CONV2D = 1, PDL_OP_GEMM = 2 };
 
 /* Convolution, raw KCRS16c16k weights.  Needs a workspace of
- * pdl_workspace_bytes(PDL_OP_CONV2D, dims, cfg) bytes (the prepacked weights),
- * dims = {N, C, K, H, W, R, S, stride, pad, flags}. */
+ * pdl_workspace_bytes(PDL_OP_CONV2D, dims, cfg) bytes (the prepacked weights,
+ * then -- 256-byte aligned -- the split-K area when the schedule splits; that
+ * area must be zero on first use), dims = {N, C, K, H, W, R, S, stride, pad, flags}. */
 int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, float *y,
                            int N, int C, int K, int H, int W, int R, int S, int stride,
                            int pad, unsigned flags, const pdl_tile_cfg *cfg, void *workspace,
@@ -99,6 +101,22 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
                              float *y, int N, int C, int K, int H, int W, int R, int S,
                              int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg,
                              void *stream);
+
+/* Split-K (small batches: a 7x7 layer at 32 images has 64 tiles for 148 SMs):
+ * the same call with a workspace, so the library may cut each tile's reduction
+ * into ranges computed by different CTAs.  Partials meet in the workspace; the
+ * last CTA of a tile sums them in range order (deterministic, independent of
+ * arrival order) and runs the fused epilogue.  The workspace (256-byte aligned,
+ * pdl_conv2d_splitk_workspace_bytes(...) bytes, 0 = this shape does not split)
+ * must be ZERO before its first use; its tile counters reset themselves, so it
+ * can be reused by later calls on the same stream (not by concurrent streams). */
+size_t pdl_conv2d_splitk_workspace_bytes(int N, int C, int K, int H, int W, int R, int S,
+                                         int stride, int pad, unsigned flags,
+                                         const pdl_tile_cfg *cfg);
+int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const float *bias,
+                                float *y, int N, int C, int K, int H, int W, int R, int S,
+                                int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg,
+                                void *workspace, size_t ws_bytes, void *stream);
 
 /* Host-buffer convolution -- the reference's interpret() contract (host arrays
  * in, fresh host arrays out: simcache.py:89-204, inputs copied at :110).
@@ -118,7 +136,9 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
                         int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg, int chunk,
                         void *workspace, size_t ws_bytes, void *stream);
 
-/* C = alpha * A B + beta * C, row-major with leading dimensions lda/ldb/ldc. */
+/* C = alpha * A B + beta * C, row-major with leading dimensions lda/ldb/ldc.
+ * workspace: optional split-K area (same rules as pdl_conv2d_fwd_prepacked_ws),
+ * pdl_workspace_bytes(PDL_OP_GEMM, {M, N, K, flags}, cfg) bytes; NULL = no split. */
 int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda,
                  int ldb, int ldc, float alpha, float beta, unsigned flags,
                  const pdl_tile_cfg *cfg, void *workspace, size_t ws_bytes, void *stream);

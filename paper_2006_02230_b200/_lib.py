@@ -10,7 +10,8 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpdl.so")
+# PDL_LIB: load another build of the library (A/B experiments between builds)
+LIB_PATH = os.environ.get("PDL_LIB") or os.path.join(_PKG, "libpdl.so")
 
 PDL_BIAS = 1
 PDL_RELU = 2
@@ -33,6 +34,7 @@ EXPORTS = (
     "pdl_workspace_bytes", "pdl_default_cfg", "pdl_last_launch_count", "pdl_last_error",
     "pdl_abi_version", "pdl_device_check", "pdl_pack_nchw16c", "pdl_unpack_nchw16c",
     "pdl_pack_kcrs16c16k", "pdl_conv2d_host_workspace_bytes", "pdl_conv2d_fwd_host",
+    "pdl_conv2d_splitk_workspace_bytes", "pdl_conv2d_fwd_prepacked_ws",
 )
 
 
@@ -84,6 +86,10 @@ def _declare(L):
     L.pdl_conv2d_prepack_weights.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
     L.pdl_conv2d_fwd_prepacked.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
         _u, ctypes.POINTER(TileCfg), _vp]
+    L.pdl_conv2d_splitk_workspace_bytes.argtypes = [_i] * 9 + [_u, ctypes.POINTER(TileCfg)]
+    L.pdl_conv2d_splitk_workspace_bytes.restype = _sz
+    L.pdl_conv2d_fwd_prepacked_ws.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
+        _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
     L.pdl_conv2d_host_workspace_bytes.argtypes = [_i] * 10
     L.pdl_conv2d_host_workspace_bytes.restype = _sz
     L.pdl_conv2d_fwd_host.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
@@ -104,7 +110,7 @@ def _declare(L):
     L.pdl_device_check.argtypes = []
     for name in EXPORTS:
         if name not in ("pdl_conv2d_packed_bytes", "pdl_workspace_bytes", "pdl_last_error",
-                        "pdl_conv2d_host_workspace_bytes"):
+                        "pdl_conv2d_host_workspace_bytes", "pdl_conv2d_splitk_workspace_bytes"):
             getattr(L, name).restype = _i
 
 

@@ -90,6 +90,13 @@ int device_check() {
 // PDL_TRACE builds: device buffer receiving block 0's event stamps (see pdl_trace_buffer).
 unsigned long long *g_trace = nullptr;
 
+// Programmatic dependent launch of the tile engine (PDL_NO_PDL=1 in the
+// environment turns it off, for A/B measurements).
+const bool g_pdl = [] {
+    const char *e = std::getenv("PDL_NO_PDL");
+    return !(e && e[0] == '1');
+}();
+
 // Reduction elements accumulated in TMEM before an fp32 round-to-nearest drain.
 constexpr int kSegElems = 256;
 // CTAs per cluster sharing (multicasting) each weight tile.
@@ -109,16 +116,21 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
     static cudaError_t attr_err = cudaSuccess;
     static int max_ctas = 0;
     cudaLaunchConfig_t lc = {};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: this grid may start (barrier init, TMEM
+    // alloc, descriptor prefetch) while the previous kernel on the stream drains;
+    // it reads / writes global memory only after griddepcontrol.wait
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     lc.blockDim = dim3(pdl::kThreads);
     lc.dynamicSmemBytes = L::TOTAL;
     lc.stream = s;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = 2;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (attr_err != cudaSuccess) return;
@@ -136,6 +148,10 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
     lc.gridDim = dim3(grid);
     pdl::TileParams pt = p;
     pt.trace = g_trace;
+    if (pt.split <= 1) {
+        pt.split = 1;
+        pt.kb_per = pt.num_kb;
+    }
     cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, pt);
     if (e != cudaSuccess) return fail(PDL_ELAUNCH, "tile_mma_kernel launch: %s", cudaGetErrorString(e));
     ++g_launches;
@@ -191,8 +207,8 @@ int dispatch_pair(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParam
 template <int KIND, bool SPLIT3>
 int dispatch_tile(int bn, int cg, int cl, const pdl::TmaMaps &maps, const pdl::TileParams &p,
                   cudaStream_t s) {
-    // work in CTAs: one per (M-tile, N-tile), rounded up to whole clusters per N-tile
-    const int work = ((p.m_tiles + cl - 1) / cl) * cl * p.n_tiles;
+    // work in CTAs: one per (M-tile, N-tile[, split]), rounded up to whole clusters per N-tile
+    const int work = ((p.m_tiles + cl - 1) / cl) * cl * p.n_tiles * std::max(1, p.split);
     if constexpr (KIND == pdl::KIND_STEM) return dispatch_bn<KIND, SPLIT3, 1>(bn, cg, maps, p, work, s);
     else {
         switch (cl) {
@@ -202,6 +218,93 @@ int dispatch_tile(int bn, int cg, int cl, const pdl::TmaMaps &maps, const pdl::T
         }
     }
     return fail(PDL_EUNSUPPORTED, "cluster size %d not in {1,2,4}", cl);
+}
+
+// ---------------------------------------------------------------- split-K
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Split-K plan: when a layer's tiles leave persistent CTAs idle (small per-GPU
+// batches: 7x7 maps at 32 images fill 64 of 148 SMs), each tile's reduction is
+// cut into `split` ranges run as separate units; partials meet in the workspace
+// [ctr: tiles ints][part: tiles x split x 128 x BN fp32].  req: cfg->split_k
+// (0 = auto, 1 = off, > 1 = forced).
+struct SplitPlan {
+    int split = 1, kb_per = 0;
+    size_t bytes = 0;
+};
+
+SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int seg_kb, int req) {
+    SplitPlan sp;
+    sp.kb_per = num_kb;
+    const int tiles = (m_tiles + cl - 1) / cl * cl * n_tiles;
+    int S = 1;
+    if (req > 1) {
+        S = std::min(req, num_kb);
+    } else if (req == 0 && tiles < sm_count) {
+        // cost ~ waves x (k-blocks per unit + fixed per-unit overhead of ~8 k-blocks:
+        // first-load latency, TMEM drain, partial write/read; small GEMMs measured
+        // slower with a 4-k-block model)
+        constexpr double kOverheadKb = 8.0;
+        double best = (double)((tiles + sm_count - 1) / sm_count) * (num_kb + kOverheadKb);
+        for (int s = 2; s <= 16; ++s) {
+            const int kps = (num_kb + s - 1) / s;
+            if (kps < 8) break;
+            const double c = (double)((tiles * s + sm_count - 1) / sm_count) * (kps + kOverheadKb) + 0.25 * s;
+            if (c < best - 1e-9) {
+                best = c;
+                S = s;
+            }
+        }
+    }
+    if (S > 1) {
+        int kps = (num_kb + S - 1) / S;
+        if (kps > seg_kb) {  // ranges on segment edges, unless that unbalances the last range
+            const int r = (kps + seg_kb - 1) / seg_kb * seg_kb;
+            if (num_kb - r * (S - 1) >= r / 2) kps = r;
+        }
+        const int split = (num_kb + kps - 1) / kps;
+        if (split > 1) {
+            sp.split = split;
+            sp.kb_per = kps;
+            sp.bytes = align256((size_t)tiles * sizeof(int)) + (size_t)tiles * split * 128 * bn * sizeof(float);
+        }
+    }
+    return sp;
+}
+
+// Bind a split plan to the caller's workspace (NULL workspace + auto = no split).
+int bind_split(pdl::TileParams &p, const SplitPlan &sp, void *ws, size_t ws_bytes, int cl) {
+    p.split = sp.split;
+    p.kb_per = sp.kb_per;
+    if (sp.split == 1) return PDL_OK;
+    if (!ws || ws_bytes < sp.bytes)
+        return fail(PDL_EWORKSPACE, "split-K x%d needs a zero-initialised workspace of %zu bytes", sp.split, sp.bytes);
+    if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(PDL_EALIGN, "split-K workspace must be 256-byte aligned");
+    const int tiles = (p.m_tiles + cl - 1) / cl * cl * p.n_tiles;
+    p.ctr = reinterpret_cast<int *>(ws);
+    p.part = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + align256((size_t)tiles * sizeof(int)));
+    return PDL_OK;
+}
+
+// GEMM tile choice (shared by the launch and the workspace query).
+void gemm_cfg(int N, const pdl_tile_cfg *cfg_in, int *bn, int *cl, int *raster) {
+    *bn = N <= 64 ? 64 : 128;
+    *raster = 0;
+    *cl = kDefaultCluster;
+    if (cfg_in) {
+        if (cfg_in->bn) *bn = cfg_in->bn;
+        if (cfg_in->cluster_m) *cl = cfg_in->cluster_m;
+        *raster = cfg_in->raster;
+    }
+}
+
+size_t gemm_split_bytes(int M, int N, int K, unsigned flags, const pdl_tile_cfg *cfg_in) {
+    if (M <= 0 || N <= 0 || K <= 0 || (flags & PDL_MODE_MASK) == PDL_MODE_FP32) return 0;
+    int bn, cl, raster;
+    gemm_cfg(N, cfg_in, &bn, &cl, &raster);
+    if (cl != 1 && cl != 2 && cl != 4) return 0;
+    return plan_split((M + 127) / 128, (N + bn - 1) / bn, cl, bn, (K + 31) / 32, kSegElems / 32,
+                      cfg_in ? cfg_in->split_k : 0).bytes;
 }
 
 // ---------------------------------------------------------------- conv geometry
@@ -369,14 +472,22 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     return dispatch_tile<pdl::KIND_STEM, false>(bn, scg, 1, maps, p, st);
 }
 
+// ws / ws_bytes: split-K workspace (may be NULL: no split unless cfg forces one).
+// query != NULL: only store the split-K workspace bytes this call would need.
 int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, int N, int C, int K,
                 int H, int W, int R, int S, int stride, int pad, unsigned flags,
-                const pdl_tile_cfg *cfg_in, cudaStream_t st) {
+                const pdl_tile_cfg *cfg_in, cudaStream_t st, void *ws = nullptr, size_t ws_bytes = 0,
+                size_t *query = nullptr) {
     int rc;
-    if ((rc = get_encode())) return rc;
     if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
-    if (is_stem(C, R, S, stride))
+    if (is_stem(C, R, S, stride)) {
+        if (query) {
+            *query = 0;
+            return PDL_OK;
+        }
+        if ((rc = get_encode())) return rc;
         return conv_fwd_stem(x, wp, bias, y, N, C, K, H, W, R, S, stride, pad, flags, cfg_in, st);
+    }
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
     conv_default_cfg(C, K, R, S, &cfg);
@@ -404,6 +515,19 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     if (cfg.bn % (8 * cl)) return fail(PDL_EINVAL, "conv: bn=%d not divisible into %d slices", cfg.bn, cl);
     if (cg < 1 || CT % cg) return fail(PDL_EINVAL, "conv: bk=%d does not divide C=%d", cfg.bk, C);
     const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad);
+    const int m_tiles = g.tiles_w * g.tiles_h * g.tiles_n, n_tiles = (K + cfg.bn - 1) / cfg.bn;
+    const int num_kb = (CT / cg) * R * S, seg_kb = std::max(1, kSegElems / (16 * cg));
+    SplitPlan spl;
+    spl.kb_per = num_kb;
+    if (!pair && !resident) {
+        const int req = cfg_in ? cfg_in->split_k : 0;
+        spl = plan_split(m_tiles, n_tiles, cl, cfg.bn, num_kb, seg_kb, (ws || query) ? req : (req > 1 ? req : 1));
+    }
+    if (query) {
+        *query = spl.bytes;
+        return PDL_OK;
+    }
+    if ((rc = get_encode())) return rc;
 
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -453,8 +577,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     }
     if ((rc = encode_y(&maps.y, y, N, KT, g.Pg, g.Qg, g.BW, g.BH, g.BNI))) return rc;
     pdl::TileParams p{};
-    p.num_kb = (CT / cg) * R * S;
-    p.seg_kb = std::max(1, kSegElems / (16 * cg));
+    p.num_kb = num_kb;
+    p.seg_kb = seg_kb;
     p.n_out = K;
     p.flags = flags;
     p.bias = bias;
@@ -473,9 +597,10 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.BNI = g.BNI;
     p.tiles_w = g.tiles_w;
     p.tiles_h = g.tiles_h;
-    p.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
+    p.m_tiles = m_tiles;
     p.raster = cfg.raster;
-    p.n_tiles = (K + cfg.bn - 1) / cfg.bn;
+    p.n_tiles = n_tiles;
+    if ((rc = bind_split(p, spl, ws, ws_bytes, cl))) return rc;
     if (pair) return dispatch_pair(cfg.bn, cg, maps, p, st);
     if (resident) {
         p.res_bytes = res_plane;
@@ -524,8 +649,6 @@ int host_chunk(int N, size_t x_img) {
     int c = (int)std::max<size_t>(1, target / std::max<size_t>(x_img, 1));
     return std::max(1, std::min(c, (N + 3) / 4));
 }
-
-size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 }  // namespace
 
@@ -588,6 +711,34 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
     if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
     return conv_fwd_tc(x, reinterpret_cast<const float *>(packed_w), bias, y, N, C, K, H, W, R, S,
                        stride, pad, flags, cfg, (cudaStream_t)stream);
+}
+
+size_t pdl_conv2d_splitk_workspace_bytes(int N, int C, int K, int H, int W, int R, int S, int stride,
+                                         int pad, unsigned flags, const pdl_tile_cfg *cfg) {
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32) return 0;
+    size_t need = 0;
+    if (conv_check(nullptr, nullptr, N, C, K, H, W, R, S, stride, pad)) return 0;
+    if (conv_fwd_tc(nullptr, nullptr, nullptr, nullptr, N, C, K, H, W, R, S, stride, pad, flags, cfg,
+                    nullptr, nullptr, 0, &need))
+        return 0;
+    return need;
+}
+
+int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const float *bias, float *y,
+                                int N, int C, int K, int H, int W, int R, int S, int stride, int pad,
+                                unsigned flags, const pdl_tile_cfg *cfg, void *workspace,
+                                size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
+    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
+        return fail(PDL_EUNSUPPORTED, "conv: PDL_MODE_FP32 takes raw weights (pdl_conv2d_fwd_nchw16c)");
+    if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
+    return conv_fwd_tc(x, reinterpret_cast<const float *>(packed_w), bias, y, N, C, K, H, W, R, S,
+                       stride, pad, flags, cfg, (cudaStream_t)stream, workspace, ws_bytes);
 }
 
 size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R, int S, int stride,
@@ -691,12 +842,16 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
         ++g_launches;
         return check_launch("simt_conv_kernel");
     }
-    const size_t need = pdl_conv2d_packed_bytes(C, K, R, S, flags);
-    if (!workspace || ws_bytes < need)
-        return fail(PDL_EWORKSPACE, "conv: workspace of %zu bytes required", need);
+    // workspace = [prepacked weights][split-K area, when the plan splits]
+    const size_t packed = pdl_conv2d_packed_bytes(C, K, R, S, flags);
+    if (!workspace || ws_bytes < packed)
+        return fail(PDL_EWORKSPACE, "conv: workspace of %zu bytes required", packed);
+    const size_t off = align256(packed);
+    void *split_ws = ws_bytes > off ? reinterpret_cast<uint8_t *>(workspace) + off : nullptr;
+    const size_t split_bytes = ws_bytes > off ? ws_bytes - off : 0;
     if ((rc = pdl_conv2d_prepack_weights(w, workspace, C, K, R, S, flags, stream))) return rc;
     rc = conv_fwd_tc(x, reinterpret_cast<const float *>(workspace), bias, y, N, C, K, H, W, R, S,
-                     stride, pad, flags, cfg, st);
+                     stride, pad, flags, cfg, st, split_ws, split_bytes);
     if (rc == PDL_OK) g_launches = 2;
     return rc;
 }
@@ -704,8 +859,6 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
 int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda, int ldb,
                  int ldc, float alpha, float beta, unsigned flags, const pdl_tile_cfg *cfg_in,
                  void *workspace, size_t ws_bytes, void *stream) {
-    (void)workspace;
-    (void)ws_bytes;
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
@@ -726,13 +879,8 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
         return check_launch("simt_gemm_kernel");
     }
     if ((rc = get_encode())) return rc;
-    int bn = N <= 64 ? 64 : 128;
-    int raster = 0, cl = kDefaultCluster;
-    if (cfg_in) {
-        if (cfg_in->bn) bn = cfg_in->bn;
-        if (cfg_in->cluster_m) cl = cfg_in->cluster_m;
-        raster = cfg_in->raster;
-    }
+    int bn, cl, raster;
+    gemm_cfg(N, cfg_in, &bn, &cl, &raster);
     if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "gemm: cluster_m must be 1, 2 or 4");
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -762,6 +910,12 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     p.raster = raster;
     p.m_tiles = (M + 127) / 128;
     p.n_tiles = (N + bn - 1) / bn;
+    {
+        const int req = cfg_in ? cfg_in->split_k : 0;
+        const SplitPlan spl = plan_split(p.m_tiles, p.n_tiles, cl, bn, p.num_kb, p.seg_kb,
+                                         workspace ? req : (req > 1 ? req : 1));
+        if ((rc = bind_split(p, spl, workspace, ws_bytes, cl))) return rc;
+    }
     if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, cl, maps, p, st);
     return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, cl, maps, p, st);
 }
@@ -837,8 +991,16 @@ int pdl_pack_kcrs16c16k(const float *src, float *dst, int K, int C, int R, int S
 size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg) {
     (void)cfg;
     if (op == PDL_OP_CONV2D && dims) {
-        // dims = {N, C, K, H, W, R, S, stride, pad, flags}
-        return pdl_conv2d_packed_bytes(dims[1], dims[2], dims[5], dims[6], (unsigned)dims[9]);
+        // dims = {N, C, K, H, W, R, S, stride, pad, flags}: prepacked weights + split-K area
+        const size_t split = pdl_conv2d_splitk_workspace_bytes(dims[0], dims[1], dims[2], dims[3], dims[4],
+                                                               dims[5], dims[6], dims[7], dims[8],
+                                                               (unsigned)dims[9], cfg);
+        const size_t packed = pdl_conv2d_packed_bytes(dims[1], dims[2], dims[5], dims[6], (unsigned)dims[9]);
+        return split ? align256(packed) + split : packed;
+    }
+    if (op == PDL_OP_GEMM && dims) {
+        // dims = {M, N, K, flags}: split-K area (0 when the GEMM fills the GPU)
+        return gemm_split_bytes(dims[0], dims[1], dims[2], (unsigned)dims[3], cfg);
     }
     return 0;
 }

@@ -37,7 +37,8 @@ enum : unsigned {
     DBG_NO_A_TMA = 1u << 8,     // producer skips the A loads
     DBG_NO_STAGE_ST = 1u << 9,  // staging warps skip the tcgen05.st into TMEM
     DBG_NO_EPI_STORE = 1u << 10,  // epilogue skips the global stores
-    DBG_NO_MMA = 1u << 11         // MMA warp commits without issuing the MMAs
+    DBG_NO_MMA = 1u << 11,        // MMA warp commits without issuing the MMAs
+    DBG_NO_GATHER = 1u << 12      // stem staging skips the halo reads (stores zeros)
 };
 
 // Geometry / epilogue parameters (by value, param space).
@@ -61,6 +62,13 @@ struct TileParams {
     int n_tiles;           // number of N tiles
     int raster;            // reserved
     int seg_kb;            // k-blocks per TMEM accumulation segment
+    // split-K: every tile's reduction is cut into `split` ranges of kb_per k-blocks,
+    // computed as separate work units; each writes its fp32 partial to part, and the
+    // last of a tile's units to arrive (ctr[tile], self-resetting) sums the partials in
+    // split order and runs the epilogue.  split == 1: no workspace is touched.
+    int split, kb_per;
+    float *part;
+    int *ctr;
     unsigned long long *trace;  // PDL_TRACE builds: per-event clock64 stamps of block 0
 };
 
@@ -375,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tmem_empty = tmem_full + 2;  // [2]
     uint64_t *wfull = tmem_empty + 2;      // stem weights landed
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
+    volatile uint32_t *split_flag = tmem_slot + 1;  // split-K: "this CTA reduces the tile"
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -386,6 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cid = blockIdx.x / CL;
     const int ncl = gridDim.x / CL;
     const int num_super = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
+    const int SPL = p.split;                 // 1 unless split-K
+    const int num_units = num_super * SPL;   // work unit u = (super-tile u / SPL, split u % SPL)
     const uint16_t cl_mask = (uint16_t)((1u << CL) - 1);
     auto tile_of = [&](int st) {  // M-tile may exceed m_tiles (phantom: loads OOB zeros, stores masked)
         const int mg = st / p.n_tiles;
@@ -429,6 +440,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (CL > 1) cluster_sync();  // peers multicast into our barriers: they must exist
     else __syncthreads();
     tc_fence_after();
+    // programmatic dependent launch: let the next kernel on the stream start its own
+    // prologue now, and touch global memory only once the previous grid has finished
+    // (a no-op when launched without the attribute)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t smem0 = smem_u32(smem);
 
@@ -472,9 +488,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
             }
-            for (int st = cid; KIND != KIND_STEM && st < num_super; st += ncl) {
+            for (int u = cid; KIND != KIND_STEM && u < num_units; u += ncl) {
+                const int st = u / SPL;
+                const int kb0 = (u - st * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
                 const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
-                for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
+                for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
                     mbar_wait(&empty[s], ph ^ 1);
                     trace_ev(p, TR_P_ISSUE, kglob);
                     uint8_t *sp = smem + s * L::STAGE;
@@ -543,10 +561,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             int g = 0, kglob = 0;
             const int num_kb = p.num_kb;
             // pairs: only the leader CTA issues (its MMAs drive both CTAs' tensor cores)
-            for (int st_i = cid; st_i < num_super && (!PAIR || rank == 0); st_i += ncl) {
+            for (int u = cid; u < num_units && (!PAIR || rank == 0); u += ncl) {
+                const int kb0 = (u - (u / SPL) * SPL) * p.kb_per, kb1 = min(num_kb, kb0 + p.kb_per);
                 int in_seg = 0;
                 uint32_t d_tmem = tmem_base;
-                for (int kb = 0; kb < num_kb; ++kb, ++kglob) {
+                for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
                     if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
                         if (PAIR) mbar_wait_cluster(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
                         else mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
@@ -646,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) trace_ev(p, TR_M_ISSUED, kglob);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if (++t == TSLOTS) { t = 0; tph ^= 1; }
-                    if (++in_seg == seg_kb || kb + 1 == num_kb) {
+                    if (++in_seg == seg_kb || kb + 1 == kb1) {
                         if constexpr (PAIR) mma_commit_pair_elect(&tmem_full[g & 1]);
                         else mma_commit_elect(&tmem_full[g & 1]);
                         in_seg = 0;
@@ -689,12 +708,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int c = 0; c < 5; ++c) {
                             float x[16], lo[16];
-                            if (kb == 0) stem_gather16_kb<0>(c, sa, row_step, live, x);
-                            else stem_gather16_kb<1>(c, sa, row_step, live, x);
+                            const bool lv = live && !(p.flags & DBG_NO_GATHER);
+                            if (kb == 0) stem_gather16_kb<0>(c, sa, row_step, lv, x);
+                            else stem_gather16_kb<1>(c, sa, row_step, lv, x);
 #pragma unroll
                             for (int i = 0; i < 16; ++i) lo[i] = tf32_lo(x[i]);
-                            tmem_st16(t_hi + c * 16, x);
-                            if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
+                            if (!(p.flags & DBG_NO_STAGE_ST)) {
+                                tmem_st16(t_hi + c * 16, x);
+                                if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
+                            }
                         }
                         if (kb + 1 == p.num_kb) mbar_arrive(&empty[s]);  // halo tile consumed
                         tmem_wait_st();
@@ -739,8 +761,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0, tph = 0;
             int kglob = 0;
             const bool tr = tid == 0;
-            for (int st_i = cid; st_i < num_super; st_i += ncl) {
-                for (int kb = 0; kb < p.num_kb; ++kb, ++kglob) {
+            for (int u = cid; u < num_units; u += ncl) {
+                const int kb0 = (u - (u / SPL) * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
+                for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
                     mbar_wait(&full[s], ph);
                     if (tr) trace_ev(p, TR_S_FULL, kglob);
                     const uint32_t sa = smem0 + s * L::STAGE + L::A_OFF;
@@ -810,11 +833,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = e >> 2;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        const int nseg = (p.num_kb + seg_kb - 1) / seg_kb;
         const bool tr = e == 0 && lane == 0;
         int g = 0, jt = 0;
         uint32_t eblk = 0;  // output boxes issued by this half (epilogue buffer ring)
-        for (int st_i = cid; st_i < num_super; st_i += ncl, ++jt) {
+        for (int u = cid; u < num_units; u += ncl, ++jt) {
+            const int st_i = u / SPL, sp = u - st_i * SPL;
+            const int kb0 = sp * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
+            const int nseg = (kb1 - kb0 + seg_kb - 1) / seg_kb;
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
             float sum[HALF];
             for (int sg = 0; sg < nseg; ++sg, ++g) {
@@ -842,6 +867,54 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (PAIR) mbar_arrive_on(&tmem_empty[g & 1], 0);
                 else mbar_arrive(&tmem_empty[g & 1]);
                 if (tr) trace_ev(p, TR_E_DRAINED, g);
+            }
+            if (SPL > 1) {
+                // ---- split-K: publish this unit's partial; the tile's last unit reduces
+                const int tile = tile_of(st_i);
+                float *mine = p.part + ((size_t)tile * SPL + sp) * (128 * BN);
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    float4 *d = reinterpret_cast<float4 *>(mine + ((half * (HALF / 16) + j) * 128 + row) * 16);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        d[q4] = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
+                                            sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
+                }
+                __threadfence();
+                named_bar_sync(4, kEpiThreads);
+                if (e == 0 && lane == 0) {
+                    const int prev = atomicAdd(p.ctr + tile, 1);
+                    const uint32_t last = prev == SPL - 1;
+                    if (last) p.ctr[tile] = 0;  // ready for the next launch
+                    *split_flag = last;
+                }
+                named_bar_sync(4, kEpiThreads);
+                if (!*split_flag) continue;
+                __threadfence();
+                // fixed split order (independent of arrival order): ((p0 + p1) + p2) + ...;
+                // this unit's own partial is read back too (registers stay free)
+                const float *tp = p.part + (size_t)tile * SPL * (128 * BN);
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    const int off = ((half * (HALF / 16) + j) * 128 + row) * 16;
+                    float4 t[4];
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) t[q4] = __ldcg(reinterpret_cast<const float4 *>(tp + off) + q4);
+#pragma unroll 1
+                    for (int q = 1; q < SPL; ++q) {
+                        const float4 *src = reinterpret_cast<const float4 *>(tp + (size_t)q * (128 * BN) + off);
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 w4 = __ldcg(src + q4);
+                            t[q4].x += w4.x; t[q4].y += w4.y; t[q4].z += w4.z; t[q4].w += w4.w;
+                        }
+                    }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        sum[j * 16 + q4 * 4] = t[q4].x; sum[j * 16 + q4 * 4 + 1] = t[q4].y;
+                        sum[j * 16 + q4 * 4 + 2] = t[q4].z; sum[j * 16 + q4 * 4 + 3] = t[q4].w;
+                    }
+                }
             }
             if constexpr (KIND != KIND_GEMM) {
                 // ---- store via TMA (bias + ReLU fused): per 16-channel block, the half's

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (PDL_BIAS, PDL_RELU, MODES, TileCfg, check, lib)
+from ._lib import (PDL_BIAS, PDL_OP_GEMM, PDL_RELU, MODES, TileCfg, check, lib)
 
 
 def _mode(mode: str) -> int:
@@ -51,6 +51,28 @@ def _cfg_ptr(cfg):
     if isinstance(cfg, dict):
         cfg = TileCfg.make(**cfg)
     return ctypes.byref(cfg)
+
+
+_split_ws: dict = {}
+_split_ws_retired: list = []
+
+
+def _split_workspace(device, stream_handle: int, nbytes: int):
+    """Zero-initialised split-K workspace, one per (device, stream): its tile
+    counters reset themselves at the end of every launch, so concurrent streams
+    must not share one.  Buffers are only ever added (a CUDA graph captured
+    earlier keeps pointing at the old one), growing 2x at a time."""
+    if nbytes == 0:
+        return None
+    key = (torch.device(device).index, stream_handle)
+    ws = _split_ws.get(key)
+    if ws is None or ws.numel() * 4 < nbytes:
+        if ws is not None:
+            _split_ws_retired.append(ws)
+            nbytes = max(nbytes, ws.numel() * 8)
+        ws = torch.zeros((nbytes + 3) // 4, dtype=torch.float32, device=device)
+        _split_ws[key] = ws
+    return ws
 
 
 def conv_out_hw(h, w, r, s, stride, pad):
@@ -119,15 +141,24 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
     _need_cuda_f32("out", y)
     flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
     st = ctypes.c_void_p(_stream(stream))
+    cp = _cfg_ptr(cfg)
     if packed is not None:
-        check(lib().pdl_conv2d_fwd_prepacked(_ptr(x), _ptr(packed.data), _ptr(bias), _ptr(y), n, C,
-                                             K, h, wd, R, S, stride, pad, flags, _cfg_ptr(cfg), st))
+        # split-K (tiles that leave SMs idle, e.g. 7x7 maps at small batches) needs a workspace
+        need = lib().pdl_conv2d_splitk_workspace_bytes(n, C, K, h, wd, R, S, stride, pad, flags, cp)
+        ws = _split_workspace(x.device, st.value or 0, need)
+        check(lib().pdl_conv2d_fwd_prepacked_ws(_ptr(x), _ptr(packed.data), _ptr(bias), _ptr(y), n,
+                                                C, K, h, wd, R, S, stride, pad, flags, cp, _ptr(ws),
+                                                need, st))
     else:
         nbytes = lib().pdl_conv2d_packed_bytes(C, K, R, S, flags)
-        ws = torch.empty(max(nbytes // 4, 4), dtype=torch.float32, device=x.device)
+        split = lib().pdl_conv2d_splitk_workspace_bytes(n, C, K, h, wd, R, S, stride, pad, flags, cp)
+        off = (nbytes + 255) // 256 * 256
+        total = off + split if split else nbytes
+        ws = torch.empty(max((total + 3) // 4, 4), dtype=torch.float32, device=x.device)
+        if split:  # fresh buffer: the split-K tile counters must start at zero
+            ws.view(torch.uint8)[off:].zero_()
         check(lib().pdl_conv2d_fwd_nchw16c(_ptr(x), _ptr(w), _ptr(bias), _ptr(y), n, C, K, h, wd,
-                                           R, S, stride, pad, flags, _cfg_ptr(cfg), _ptr(ws),
-                                           nbytes, st))
+                                           R, S, stride, pad, flags, cp, _ptr(ws), total, st))
     return y
 
 
@@ -198,9 +229,13 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha:
         c = torch.empty((m, n), dtype=torch.float32, device=a.device)
     _need_cuda_f32("c", c)
     flags = _mode(mode) | (PDL_RELU if relu else 0)
+    cp = _cfg_ptr(cfg)
+    sh = _stream(stream)
+    dims = (ctypes.c_int * 4)(m, n, k, flags)
+    need = lib().pdl_workspace_bytes(PDL_OP_GEMM, dims, cp)
+    ws = _split_workspace(a.device, sh, need)
     check(lib().pdl_gemm_f32(_ptr(a), _ptr(b), _ptr(c), m, n, k, k, n, n, float(alpha),
-                             float(beta), flags, _cfg_ptr(cfg), None, 0,
-                             ctypes.c_void_p(_stream(stream))))
+                             float(beta), flags, cp, _ptr(ws), need, ctypes.c_void_p(sh)))
     return c
 
 

@@ -50,8 +50,25 @@ def test_workspace_and_packed_bytes():
     # other narrow shapes: one k-block (8 taps x 4 channels) per kernel row
     assert L.pdl_conv2d_packed_bytes(4, 64, 7, 7, _lib.PDL_MODE_TF32) == 7 * 8 * 64 * 4 * 4
     assert L.pdl_conv2d_packed_bytes(3, 64, 5, 5, _lib.PDL_MODE_3XTF32) == 2 * 5 * 8 * 64 * 4 * 4
-    dims = (ctypes.c_int * 10)(2, 64, 128, 14, 14, 3, 3, 1, 1, 0)
+    # a batch that fills the GPU: the workspace is just the packed weights
+    dims = (ctypes.c_int * 10)(256, 64, 128, 14, 14, 3, 3, 1, 1, 0)
+    assert L.pdl_conv2d_splitk_workspace_bytes(256, 64, 128, 14, 14, 3, 3, 1, 1, 0, None) == 0
     assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 64 * 128 * 9 * 4
+    # 2 images -> 4 tiles of 128 px, 18 k-blocks: split-K x2 (two ranges of 9 k-blocks);
+    # area = 256 B of tile counters + 4 tiles x 2 ranges x 128 x 128 fp32 partials
+    split = 256 + 4 * 2 * 128 * 128 * 4
+    assert L.pdl_conv2d_splitk_workspace_bytes(2, 64, 128, 14, 14, 3, 3, 1, 1, 0, None) == split
+    dims = (ctypes.c_int * 10)(2, 64, 128, 14, 14, 3, 3, 1, 1, 0)
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 64 * 128 * 9 * 4 + split
+    # split_k = 1 turns it off; the stem never splits
+    off = _lib.TileCfg.make(split_k=1)
+    assert L.pdl_conv2d_splitk_workspace_bytes(2, 64, 128, 14, 14, 3, 3, 1, 1, 0, ctypes.byref(off)) == 0
+    assert L.pdl_conv2d_splitk_workspace_bytes(1, 3, 64, 224, 224, 7, 7, 2, 3, 0, None) == 0
+    # GEMM: 4096^3 fills the GPU; 1024^3 (64 tiles) splits in two
+    g = (ctypes.c_int * 4)(4096, 4096, 4096, 0)
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_GEMM, g, None) == 0
+    g = (ctypes.c_int * 4)(1024, 1024, 1024, 0)
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_GEMM, g, None) == 256 + 64 * 2 * 128 * 128 * 4
 
 
 def test_no_gpu_is_a_loud_error():

@@ -218,11 +218,11 @@ def test_cluster_multicast_conv(P, layer, cluster):
     ys = []
     for mode in ("3xtf32", "tf32"):
         y = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=layer.stride, pad=layer.pad,
-                             relu=True, mode=mode, cfg={"cluster_m": cluster})
+                             relu=True, mode=mode, cfg={"cluster_m": cluster, "split_k": 1})
         assert rel(y.cpu().numpy(), ref) <= TOL[mode]
         ys.append(y)
     y1 = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), stride=layer.stride, pad=layer.pad,
-                          relu=True, cfg={"cluster_m": 1})
+                          relu=True, cfg={"cluster_m": 1, "split_k": 1})
     assert torch.equal(ys[0], y1)
 
 
