@@ -418,10 +418,29 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
         }
         if (!BW) return fail(PDL_EUNSUPPORTED, "stem: no halo tile fits (S=%d R=%d)", S, R);
     }
-    const int box_w = (BW - 1) * stride + S, box_h = (BH - 1) * stride + R;
+    int box_w = (BW - 1) * stride + S;
+    const int box_h = (BH - 1) * stride + R;
+    // packed stride-2 stem: the halo is loaded as two dense boxes, even and odd input
+    // columns (BW + (S+1)/2 - 1 pixels each), so one tap's pixels are contiguous in smem
+    const bool parity = stem_packed(C, R, S) && stride == 2;
+    int halo_odd = 0;
+    if (parity) {
+        box_w = BW - 1 + (S + 1) / 2;
+        halo_odd = (box_w * box_h * 16 + 127) / 128 * 128;
+        if (2 * halo_odd > pdl::kStemHaloBytes) return fail(PDL_EUNSUPPORTED, "stem: halo too large");
+    }
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
-    {
+    if (parity) {
+        for (int par = 0; par < 2; ++par) {
+            const cuuint64_t dims[5] = {16, (cuuint64_t)((W - par + 1) / 2), (cuuint64_t)H, 1, (cuuint64_t)N};
+            const cuuint64_t str[4] = {128, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
+            const cuuint32_t box[5] = {4, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
+            if ((rc = encode(&maps.a[par], x + par * 16, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             "stem x parity", CU_TENSOR_MAP_L2_PROMOTION_NONE)))
+                return rc;
+        }
+    } else {
         const cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
         const cuuint64_t str[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
         const cuuint32_t box[5] = {4, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
@@ -462,6 +481,7 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     p.BNI = 1;
     p.box_w = box_w;
     p.box_h = box_h;
+    p.halo_odd = halo_odd;
     p.tiles_w = (Q + BW - 1) / BW;
     p.tiles_h = (P + BH - 1) / BH;
     p.m_tiles = p.tiles_w * p.tiles_h * N;

@@ -57,6 +57,8 @@ struct TileParams {
     int BW, BH, BNI;       // box of output pixels per tile
     int tiles_w, tiles_h;  // tile grid over (Q, P); images fastest-after
     int box_w, box_h;      // stem: halo tile (input pixels x input rows) of one output tile
+    int halo_odd;          // packed stride-2 stem: byte offset of the odd-column halo region
+                           // (0: one contiguous halo box)
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
@@ -323,40 +325,36 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     return c;
 }
 
-// Packed ResNet-stem gather (C=3, R=S=7): reduction index k = (r*7 + s)*3 + c
-// (147 real, zero beyond).  Values K0..K0+15: one 16-byte halo load per (r, s)
-// tap, shared by the k-values it feeds; everything is compile-time but the
-// halo addresses.
-template <int K0>
-__device__ __forceinline__ void stem_gather16(uint32_t sa, uint32_t row_step, bool live, float (&x)[16]) {
-    constexpr int rs_lo = K0 / 3;
-    constexpr int rs_hi0 = (K0 + 15) / 3;
-    constexpr int rs_hi = rs_hi0 < 48 ? rs_hi0 : 48;
+// Packed ResNet-stem gather (C=3, R=S=7), tap-aligned: reduction chunk CH (0..9)
+// of 16 values holds taps 5*CH .. 5*CH+4 (tap = r*7 + s, 3 channels each) and a
+// zero, so every tap is read from the halo exactly once per tile (147 real
+// values of 160).  col[s] = byte offset of tap column s for this thread (the
+// stride-2 halo is split into even / odd input-column regions, so the 16-byte
+// pixels a warp reads for one tap are contiguous: 4 smem wavefronts, not 8).
+template <int CH>
+__device__ __forceinline__ void stem_gather_chunk(uint32_t sa, uint32_t row_step, const uint32_t (&col)[7],
+                                                  bool live, float (&x)[16]) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = 0.f;
-#pragma unroll
-    for (int rs = rs_lo; rs <= rs_hi; ++rs) {
-        const int r = rs / 7, s = rs - (rs / 7) * 7;
+    for (int i = 0; i < 5; ++i) {
+        const int tap = 5 * CH + i;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (live) v = lds128(sa + r * row_step + s * 16);
-        const float vv[3] = {v.x, v.y, v.z};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int k = rs * 3 + c - K0;
-            if (k >= 0 && k < 16) x[k] = vv[c];
-        }
+        if (tap < 49 && live) v = lds128(sa + (uint32_t)(tap / 7) * row_step + col[tap % 7]);
+        x[3 * i] = v.x;
+        x[3 * i + 1] = v.y;
+        x[3 * i + 2] = v.z;
     }
+    x[15] = 0.f;
 }
-// chunk c (0..4) of packed k-block KB (80 values each)
+// chunk c (0..4) of packed k-block KB (5 chunks = 80 values each)
 template <int KB>
-__device__ __forceinline__ void stem_gather16_kb(int c, uint32_t sa, uint32_t row_step, bool live,
-                                                 float (&x)[16]) {
+__device__ __forceinline__ void stem_gather_kb(int c, uint32_t sa, uint32_t row_step, const uint32_t (&col)[7],
+                                               bool live, float (&x)[16]) {
     switch (c) {
-        case 0: stem_gather16<KB * 80 + 0>(sa, row_step, live, x); break;
-        case 1: stem_gather16<KB * 80 + 16>(sa, row_step, live, x); break;
-        case 2: stem_gather16<KB * 80 + 32>(sa, row_step, live, x); break;
-        case 3: stem_gather16<KB * 80 + 48>(sa, row_step, live, x); break;
-        default: stem_gather16<KB * 80 + 64>(sa, row_step, live, x); break;
+        case 0: stem_gather_chunk<KB * 5 + 0>(sa, row_step, col, live, x); break;
+        case 1: stem_gather_chunk<KB * 5 + 1>(sa, row_step, col, live, x); break;
+        case 2: stem_gather_chunk<KB * 5 + 2>(sa, row_step, col, live, x); break;
+        case 3: stem_gather_chunk<KB * 5 + 3>(sa, row_step, col, live, x); break;
+        default: stem_gather_chunk<KB * 5 + 4>(sa, row_step, col, live, x); break;
     }
 }
 
@@ -456,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else if (KIND == KIND_CONV)
                 tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
                                 (RESW ? 0 : G::B_BYTES * L::LOAD_PLANES));
-            else tx = (uint32_t)(16 * p.box_w * p.box_h);
+            else tx = (uint32_t)(16 * p.box_w * p.box_h * (p.halo_odd ? 2 : 1));
             if (RESW && blockIdx.x < num_tiles) {
                 // the grid is a multiple of n_tiles: this CTA keeps one N-tile throughout
                 const int n0 = (blockIdx.x % p.n_tiles) * BN;
@@ -483,8 +481,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], ph ^ 1);
                     trace_ev(p, TR_P_ISSUE, kglob);
                     mbar_arrive_expect_tx(&full[s], tx);
-                    tma_load_5d(smem + s * L::STAGE + L::A_OFF, &maps.a[0], &full[s], 0,
-                                tc.q0 * p.stride - p.pad, tc.p0 * p.stride - p.pad, 0, tc.i0);
+                    const int c0 = tc.q0 * p.stride - p.pad;  // first input column of the halo
+                    if (p.halo_odd) {
+                        // stride 2: even and odd input columns as two dense boxes
+                        // (a[0] / a[1] index columns 2k / 2k+1)
+                        tma_load_5d(smem + s * L::STAGE + L::A_OFF, &maps.a[0], &full[s], 0,
+                                    (c0 + (c0 & 1)) / 2, tc.p0 * p.stride - p.pad, 0, tc.i0);
+                        tma_load_5d(smem + s * L::STAGE + L::A_OFF + p.halo_odd, &maps.a[1], &full[s], 0,
+                                    (c0 - (c0 & 1)) / 2, tc.p0 * p.stride - p.pad, 0, tc.i0);
+                    } else {
+                        tma_load_5d(smem + s * L::STAGE + L::A_OFF, &maps.a[0], &full[s], 0, c0,
+                                    tc.p0 * p.stride - p.pad, 0, tc.i0);
+                    }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
             }
@@ -687,8 +695,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool live = row < p.BW * p.BH;
             const int ph_ = live ? row / p.BW : 0;
             const int pw_ = live ? row - ph_ * p.BW : 0;
-            const uint32_t pix0 = (uint32_t)((ph_ * p.stride) * p.box_w + pw_ * p.stride) * 16;
+            uint32_t pix0 = (uint32_t)((ph_ * p.stride) * p.box_w + pw_ * p.stride) * 16;
             const uint32_t row_step = (uint32_t)p.box_w * 16;
+            // packed stem: byte offset of tap column s (see stem_gather_chunk)
+            uint32_t col[7];
+            if (p.halo_odd) {
+                pix0 = (uint32_t)((ph_ * 2) * p.box_w + pw_) * 16;
+                const int c0 = -p.pad;  // column parity pattern is the same for every tile
+                const int e0 = (c0 + (c0 & 1)) / 2, o0 = (c0 - (c0 & 1)) / 2;
+#pragma unroll
+                for (int sx = 0; sx < 7; ++sx) {
+                    const int cc = c0 + sx;
+                    col[sx] = (cc & 1) ? (uint32_t)p.halo_odd + (uint32_t)((cc - 1) / 2 - o0) * 16
+                                       : (uint32_t)(cc / 2 - e0) * 16;
+                }
+            } else {
+#pragma unroll
+                for (int sx = 0; sx < 7; ++sx) col[sx] = (uint32_t)sx * 16;
+            }
             int s = 0, t = 0;
             uint32_t ph = 0, tph = 0;
             int kglob = 0;
@@ -709,8 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int c = 0; c < 5; ++c) {
                             float x[16], lo[16];
                             const bool lv = live && !(p.flags & DBG_NO_GATHER);
-                            if (kb == 0) stem_gather16_kb<0>(c, sa, row_step, lv, x);
-                            else stem_gather16_kb<1>(c, sa, row_step, lv, x);
+                            if (kb == 0) stem_gather_kb<0>(c, sa, row_step, col, lv, x);
+                            else stem_gather_kb<1>(c, sa, row_step, col, lv, x);
 #pragma unroll
                             for (int i = 0; i < 16; ++i) lo[i] = tf32_lo(x[i]);
                             if (!(p.flags & DBG_NO_STAGE_ST)) {
@@ -1159,8 +1183,8 @@ __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__res
 // Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[plane][kchunk][k][4]
 // (no-swizzle K-major core matrices, 4 reduction values per 16-byte chunk).
 // Unpacked: chunk = r*8 + tap, value = channel (taps >= S and channels >= C_real
-// zero).  Packed (C=3, 7x7): value j of chunk kc is reduction index
-// q = 4kc + j = (r*S + s)*C + c, zero for q >= R*S*C.
+// zero).  Packed (C=3, 7x7): reduction index q = 4kc + j sits in tap-aligned
+// 16-value group q/16 = taps 5*(q/16) .. +4, three channels each, value 15 zero.
 __global__ void prepack_stem_weights_kernel(const float *__restrict__ w, float *__restrict__ out,
                                             int K, int R, int S, int split, int C_real, int nchunks,
                                             int packed) {
@@ -1174,12 +1198,15 @@ __global__ void prepack_stem_weights_kernel(const float *__restrict__ w, float *
         int r, tap, c;
         bool ok;
         if (packed) {
+            // tap-aligned chunks of 16: value jj of chunk ch = tap 5*ch + jj/3, channel
+            // jj%3 (jj = 15 and taps >= R*S are zero) -- matches stem_gather_chunk
             const int q = kc * 4 + j;
-            ok = q < R * S * C_real;
-            const int rs = q / C_real;
-            c = q - rs * C_real;
-            r = rs / S;
-            tap = rs - r * S;
+            const int ch = q >> 4, jj = q & 15;
+            const int t = 5 * ch + jj / 3;
+            c = jj % 3;
+            ok = jj < 15 && t < R * S && c < C_real;
+            r = t / S;
+            tap = t - r * S;
         } else {
             r = kc / 8;
             tap = kc % 8;
