@@ -59,8 +59,14 @@ typedef struct pdl_tile_cfg {
     int cluster_n; /* 2: CTA-pair tiles, cta_group::2 MMAs with M = 256 (3xTF32 conv) */
     int split_k;   /* 0: auto (split the reduction when the tiles leave SMs idle
                       and a workspace is given), 1: off, >1: that many ranges   */
-    int raster;    /* 0: M-tiles fastest, 1: N-tiles fastest                    */
+    int raster;    /* bit 0: reserved (tile order); bit 1 (PDL_RASTER_BOX_TILES):
+                      box tiles only -- no multi-image segment tiles for small maps;
+                      bit 2 (PDL_RASTER_SEG_TILES): segment tiles whenever the shape
+                      allows, even if they do not remove a wave of tiles       */
 } pdl_tile_cfg;
+
+#define PDL_RASTER_BOX_TILES 2
+#define PDL_RASTER_SEG_TILES 4
 
 enum {
     PDL_BIAS = 1,             /* y += bias[k]                                  */

@@ -245,7 +245,9 @@ SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int s
         // first-load latency, TMEM drain, partial write/read; small GEMMs measured
         // slower with a 4-k-block model)
         constexpr double kOverheadKb = 8.0;
-        double best = (double)((tiles + sm_count - 1) / sm_count) * (num_kb + kOverheadKb);
+        // a split must win by > 15% under the model (marginal wins measured as losses:
+        // ResNet layer 12 at 32 images, 100 tiles, x4 predicted 1% faster, ran 1.6x slower)
+        double best = 0.85 * (double)((tiles + sm_count - 1) / sm_count) * (num_kb + kOverheadKb);
         for (int s = 2; s <= 16; ++s) {
             const int kps = (num_kb + s - 1) / s;
             if (kps < 8) break;
@@ -314,9 +316,14 @@ struct ConvGeom {
     int Pg, Qg;
     bool flat;
     int BW, BH, BNI, tiles_w, tiles_h, tiles_n;
+    int m_tiles;
+    // segment tiles (see TileParams): 0 = box tiles
+    int seg_mode = 0, seg_tile = 0;
 };
 
-ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad) {
+// n_tiles: output-channel tiles (segment tiles only pay when they cut whole waves).
+ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool allow_seg = true,
+                   int n_tiles = 1, bool force_seg = false) {
     ConvGeom g{};
     g.P = (H + 2 * pad - R) / stride + 1;
     g.Q = (W + 2 * pad - S) / stride + 1;
@@ -331,6 +338,39 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad) {
     g.tiles_w = (g.Qg + g.BW - 1) / g.BW;
     g.tiles_h = (g.Pg + g.BH - 1) / g.BH;
     g.tiles_n = (N + g.BNI - 1) / g.BNI;
+    g.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
+    // Segment tiles: small maps waste rows in box tiles (14x14: 126 + 70 of 256 rows per
+    // image).  A segment tile is T = 128 / Q consecutive output rows of the (image, row)
+    // sequence, loaded as <= 2 exact-height boxes (end of one image, start of the next) at a
+    // 128-byte-aligned smem offset (needs Q even), so tiles span images and fill T*Q rows.
+    // Only boxes of the parity-0 map (stride 1, or 1x1 / pad 0 stride 2), T <= 10 row
+    // counts, and P >= T (a tile touches at most two images).
+    if (allow_seg && g.Q % 2 == 0 && g.Q >= 128 / pdl::kSegMaxRows && g.Q <= 64 &&
+        (stride == 1 || (R == 1 && S == 1 && pad == 0))) {
+        const int T = 128 / g.Q;
+        const long long rows = (long long)N * g.P;
+        const long long mt = (rows + T - 1) / T;
+        // only when it removes whole waves of the persistent grid: within one wave the
+        // per-tile latency is what counts, and a tile spanning two images issues two boxes
+        // per k-block (measured 2-6% slower at 32-64 images when the wave count is unchanged)
+        const long long wave = sm_count;
+        const long long w_box = ((long long)g.m_tiles * n_tiles + wave - 1) / wave;
+        const long long w_seg = (mt * n_tiles + wave - 1) / wave;
+        if (g.P >= T && T <= pdl::kSegMaxRows && (w_seg < w_box || (force_seg && mt < g.m_tiles)) &&
+            mt < (1ll << 30)) {
+            g.seg_mode = 1;
+            g.seg_tile = T;
+            g.m_tiles = (int)mt;
+            g.flat = false;
+            g.Hg = H;
+            g.Wg = W;
+            g.Pg = g.P;
+            g.Qg = g.Q;
+            g.BW = g.Q;  // epilogue / transaction bytes: T rows of Q pixels
+            g.BH = T;
+            g.BNI = 1;
+        }
+    }
     return g;
 }
 
@@ -459,7 +499,7 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
         if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
             return rc;
     }
-    if ((rc = encode_y(&maps.y, y, N, K / 16, P, Q, BW, BH, 1))) return rc;
+    if ((rc = encode_y(&maps.y[0], y, N, K / 16, P, Q, BW, BH, 1))) return rc;
     pdl::TileParams p{};
     p.num_kb = stem_kblocks(C, R, S);
     p.seg_kb = std::max(1, kSegElems / (4 * stem_chunks_per_kb(C, R, S)));
@@ -528,14 +568,21 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     const bool resident = split && !pair && R == 1 && S == 1 && cfg.bk == 32 && res_plane <= 65536 &&
                           (!cfg_in || cfg_in->cluster_m <= 1);
     if (resident) cfg.cluster_m = 1;
-    const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16, cl = cfg.cluster_m;
+    const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16;
+    int cl = cfg.cluster_m;
     const int G = weight_group(C);
     if ((G == 32) != (cg >= 2)) return fail(PDL_EINVAL, "conv: bk=%d incompatible with C=%d", cfg.bk, C);
     if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "conv: cluster_m must be 1, 2 or 4");
     if (cfg.bn % (8 * cl)) return fail(PDL_EINVAL, "conv: bn=%d not divisible into %d slices", cfg.bn, cl);
     if (cg < 1 || CT % cg) return fail(PDL_EINVAL, "conv: bk=%d does not divide C=%d", cfg.bk, C);
-    const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad);
-    const int m_tiles = g.tiles_w * g.tiles_h * g.tiles_n, n_tiles = (K + cfg.bn - 1) / cfg.bn;
+    const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad,
+                                 !pair && !(cfg_in && (cfg_in->raster & PDL_RASTER_BOX_TILES)),
+                                 (K + cfg.bn - 1) / cfg.bn, cfg_in && (cfg_in->raster & PDL_RASTER_SEG_TILES));
+    // segment tiles: no weight multicast by default (pairs of CTAs in lockstep wait for
+    // the one whose tile spans two images; cluster 1 measured 4-9% faster on ResNet
+    // layers 12/13/15 at 256 images)
+    if (g.seg_mode && !(cfg_in && cfg_in->cluster_m)) cl = 1;
+    const int m_tiles = g.m_tiles, n_tiles = (K + cfg.bn - 1) / cfg.bn;
     const int num_kb = (CT / cg) * R * S, seg_kb = std::max(1, kSegElems / (16 * cg));
     SplitPlan spl;
     spl.kb_per = num_kb;
@@ -552,7 +599,19 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
-    if (stride == 1) {
+    if (g.seg_mode) {
+        // one A map and one y map per box height 1..T (parity-0 view for stride 2)
+        const int Wv = stride == 1 ? W : (W + 1) / 2, Hv = stride == 1 ? H : (H + 1) / 2;
+        const cuuint64_t cs = stride == 1 ? 64 : 128, rs = stride == 1 ? (cuuint64_t)W * 64 : (cuuint64_t)W * 128;
+        const cuuint64_t dims[5] = {16, (cuuint64_t)Wv, (cuuint64_t)Hv, (cuuint64_t)CT, (cuuint64_t)N};
+        const cuuint64_t str[4] = {cs, rs, (cuuint64_t)H * W * 64, (cuuint64_t)CT * H * W * 64};
+        for (int h = 1; h <= g.seg_tile; ++h) {
+            const cuuint32_t box[5] = {16, (cuuint32_t)g.Q, (cuuint32_t)h, 1, 1};
+            if ((rc = encode(&maps.a[h - 1], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B, "conv x rows")))
+                return rc;
+            if ((rc = encode_y(&maps.y[h - 1], y, N, KT, g.P, g.Q, g.Q, h, 1))) return rc;
+        }
+    } else if (stride == 1) {
         const cuuint64_t dims[5] = {16, (cuuint64_t)g.Wg, (cuuint64_t)g.Hg, (cuuint64_t)CT, (cuuint64_t)N};
         const cuuint64_t str[4] = {64, (cuuint64_t)g.Wg * 64, (cuuint64_t)g.Hg * g.Wg * 64,
                                    (cuuint64_t)CT * g.Hg * g.Wg * 64};
@@ -595,7 +654,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                          G == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, "conv w")))
             return rc;
     }
-    if ((rc = encode_y(&maps.y, y, N, KT, g.Pg, g.Qg, g.BW, g.BH, g.BNI))) return rc;
+    if (!g.seg_mode && (rc = encode_y(&maps.y[0], y, N, KT, g.Pg, g.Qg, g.BW, g.BH, g.BNI))) return rc;
     pdl::TileParams p{};
     p.num_kb = num_kb;
     p.seg_kb = seg_kb;
@@ -617,6 +676,9 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.BNI = g.BNI;
     p.tiles_w = g.tiles_w;
     p.tiles_h = g.tiles_h;
+    p.seg_mode = g.seg_mode;
+    p.seg_tile = g.seg_tile;
+    p.seg_bytes = g.Q * 64;
     p.m_tiles = m_tiles;
     p.raster = cfg.raster;
     p.n_tiles = n_tiles;

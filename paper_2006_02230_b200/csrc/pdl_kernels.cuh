@@ -59,6 +59,11 @@ struct TileParams {
     int box_w, box_h;      // stem: halo tile (input pixels x input rows) of one output tile
     int halo_odd;          // packed stride-2 stem: byte offset of the odd-column halo region
                            // (0: one contiguous halo box)
+    // segment tiles (conv, small even-width maps): an M tile is seg_tile consecutive output
+    // rows of the (image, row) sequence -- the end of one image and the start of the next --
+    // loaded as two exact-height boxes stacked at a 128-byte-aligned smem offset (TMA swizzles
+    // by absolute smem address, so the stack is the canonical SW64 tile).  0: box tiles.
+    int seg_mode, seg_tile, seg_bytes;
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
@@ -103,10 +108,13 @@ __device__ __forceinline__ void trace_ev(const TileParams &p, int ev, int i) {
 #endif
 }
 
+constexpr int kSegMaxRows = 10;  // segment tiles: one box map per row count 1..10
 struct TmaMaps {
-    CUtensorMap a[4];  // conv: one per (row, col) parity for stride 2; GEMM / stem: a[0]
+    // conv box tiles: a[parity] ((row, col) parity map for stride 2, a[0] for stride 1);
+    // conv segment tiles: a[h - 1] = box of h output rows; GEMM / stem: a[0..1]
+    CUtensorMap a[kSegMaxRows];
     CUtensorMap b;
-    CUtensorMap y;     // conv / stem output [N][KT][P][Q][16] (TMA-stored epilogue)
+    CUtensorMap y[kSegMaxRows];  // conv / stem output [N][KT][P][Q][16] (TMA-stored epilogue)
 };
 
 // Shared-memory tiles of one pipeline stage.
@@ -312,6 +320,11 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     c.i0 = 0;
     if (KIND == KIND_GEMM) {
         c.m0 = mt * 128;
+    } else if (p.seg_mode) {
+        // segment tiles: output rows [mt * seg_tile, +seg_tile) of the (image, row) sequence
+        const int g0 = mt * p.seg_tile;
+        c.i0 = g0 / p.P;
+        c.p0 = g0 - c.i0 * p.P;
     } else {
         int t = mt;
         const int tw = t % p.tiles_w;
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&maps.b);
         tma_prefetch(&maps.a[0]);
-        if (KIND == KIND_CONV && p.stride == 2) {
+        if (KIND == KIND_CONV && p.stride == 2 && !p.seg_mode) {
             tma_prefetch(&maps.a[1]);
             tma_prefetch(&maps.a[2]);
             tma_prefetch(&maps.a[3]);
@@ -528,7 +541,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                             dh = (dh - ph2) >> 1;
                             dw = (dw - pw2) >> 1;
                         }
-                        if (!(p.flags & DBG_NO_A_TMA)) {
+                        if (p.flags & DBG_NO_A_TMA) {
+                        } else if (p.seg_mode) {
+                            // rows p0.. of image i0 (h1 rows), then rows 0.. of image i0 + 1
+                            const int h1 = min(p.seg_tile, p.P - tc.p0), h2 = p.seg_tile - h1;
+#pragma unroll
+                            for (int c = 0; c < CG; ++c) {
+                                uint8_t *dst = sp + L::A_OFF + c * G::A_SUB;
+                                tma_load_5d(dst, &maps.a[h1 - 1], &full[s], 0, dw, tc.p0 + dh, ctg * CG + c, tc.i0);
+                                if (h2)
+                                    tma_load_5d(dst + h1 * p.seg_bytes, &maps.a[h2 - 1], &full[s], 0, dw, dh,
+                                                ctg * CG + c, tc.i0 + 1);
+                            }
+                        } else {
 #pragma unroll
                             for (int c = 0; c < CG; ++c)
                                 tma_load_5d(sp + L::A_OFF + c * G::A_SUB, &maps.a[mi], &full[s], 0,
@@ -977,8 +1002,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     fence_proxy_async_smem();
                     named_bar_sync(2 + half, 128);
                     if (leader) {
-                        if (col0 < p.n_out && !(p.flags & DBG_NO_EPI_STORE))
-                            tma_store_5d(&maps.y, ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
+                        if (col0 >= p.n_out || (p.flags & DBG_NO_EPI_STORE)) {
+                        } else if (p.seg_mode) {
+                            const int h1 = min(p.seg_tile, p.P - tc.p0), h2 = p.seg_tile - h1;
+                            tma_store_5d(&maps.y[h1 - 1], ebuf, 0, 0, tc.p0, col0 >> 4, tc.i0);
+                            if (h2)
+                                tma_store_5d(&maps.y[h2 - 1], ebuf + h1 * p.seg_bytes, 0, 0, 0, col0 >> 4,
+                                             tc.i0 + 1);
+                        } else {
+                            tma_store_5d(&maps.y[0], ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
+                        }
                         bulk_commit();  // one group per block (possibly empty): uniform ring
                     }
                 }

@@ -1,0 +1,44 @@
+"""Segment vs box tiles per layer and batch, isolated (CUDA-graph replay of 10 launches)."""
+import sys
+
+import torch
+
+sys.path.insert(0, '.')
+import paper_2006_02230_b200 as P
+from paper_2006_02230_b200 import workloads as W
+
+idxs = [int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else [11, 12, 13, 14, 15]
+batches = [int(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else [32, 64, 256]
+cfgs = {"seg": {}, "box": {"raster": 2}, "seg_cl1": {"cluster_m": 1}, "box_cl1": {"cluster_m": 1, "raster": 2},
+        "seg_nosplit": {"split_k": 1}, "box_nosplit": {"split_k": 1, "raster": 2}}
+for n in batches:
+    for idx in idxs:
+        l = W.LAYERS[idx - 1]
+        x = torch.rand((n, l.C_alloc // 16, l.H, l.W, 16), device='cuda')
+        w = torch.rand((l.K // 16, l.C_alloc // 16, l.R, l.S, 16, 16), device='cuda')
+        b = torch.rand(l.K, device='cuda')
+        pw = P.prepack_weights(w, channels=l.C)
+        y = torch.empty((n, l.K // 16, l.P, l.Q, 16), device='cuda')
+        res = []
+        for name, cfg in cfgs.items():
+            def call():
+                P.conv2d_nchw16c(x, pw, b, stride=l.stride, pad=l.pad, relu=True, out=y, cfg=cfg or None)
+            call()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(10):
+                        call()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            res.append(f"{name}={e0.elapsed_time(e1) / 50 * 1e3:.1f}us")
+        print(f"n={n} {l.name()}: " + " ".join(res), flush=True)
