@@ -318,7 +318,7 @@ struct ConvGeom {
     int BW, BH, BNI, tiles_w, tiles_h, tiles_n;
     int m_tiles;
     // segment tiles (see TileParams): 0 = box tiles
-    int seg_mode = 0, seg_tile = 0;
+    int seg_mode = 0, seg_tile = 0, seg_imgs = 1;
 };
 
 // n_tiles: output-channel tiles (segment tiles only pay when they cut whole waves).
@@ -340,35 +340,39 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool 
     g.tiles_n = (N + g.BNI - 1) / g.BNI;
     g.m_tiles = g.tiles_w * g.tiles_h * g.tiles_n;
     // Segment tiles: small maps waste rows in box tiles (14x14: 126 + 70 of 256 rows per
-    // image).  A segment tile is T = 128 / Q consecutive output rows of the (image, row)
-    // sequence, loaded as <= 2 exact-height boxes (end of one image, start of the next) at a
-    // 128-byte-aligned smem offset (needs Q even), so tiles span images and fill T*Q rows.
-    // Only boxes of the parity-0 map (stride 1, or 1x1 / pad 0 stride 2), T <= 10 row
-    // counts, and P >= T (a tile touches at most two images).
-    if (allow_seg && g.Q % 2 == 0 && g.Q >= 128 / pdl::kSegMaxRows && g.Q <= 64 &&
-        (stride == 1 || (R == 1 && S == 1 && pad == 0))) {
-        const int T = 128 / g.Q;
-        const long long rows = (long long)N * g.P;
-        const long long mt = (rows + T - 1) / T;
-        // only when it removes whole waves of the persistent grid: within one wave the
-        // per-tile latency is what counts, and a tile spanning two images issues two boxes
-        // per k-block (measured 2-6% slower at 32-64 images when the wave count is unchanged)
-        const long long wave = sm_count;
-        const long long w_box = ((long long)g.m_tiles * n_tiles + wave - 1) / wave;
-        const long long w_seg = (mt * n_tiles + wave - 1) / wave;
-        if (g.P >= T && T <= pdl::kSegMaxRows && (w_seg < w_box || (force_seg && mt < g.m_tiles)) &&
-            mt < (1ll << 30)) {
-            g.seg_mode = 1;
-            g.seg_tile = T;
-            g.m_tiles = (int)mt;
-            g.flat = false;
-            g.Hg = H;
-            g.Wg = W;
-            g.Pg = g.P;
-            g.Qg = g.Q;
-            g.BW = g.Q;  // epilogue / transaction bytes: T rows of Q pixels
-            g.BH = T;
-            g.BNI = 1;
+    // image; 7x7: 98 of 128).  A segment tile is T consecutive bands of the (image group,
+    // output row) sequence; a band is one output row of one image (Q even) or of two images
+    // (Q odd), so every band is a whole number of 128-byte smem rows.  The tile loads as up
+    // to three exact-height boxes {Q, h, images}, so tiles span images and fill T bands of
+    // up to 128 pixels.  Only the parity-0 map is used (stride 1, or 1x1 / pad 0 stride 2),
+    // and T <= kSegMaxRows box heights.
+    {
+        const int gi = (g.Q % 2) ? 2 : 1;     // images per band
+        const int band = gi * g.Q;            // pixels per band
+        const int T = band <= 128 ? 128 / band : 0;
+        if (allow_seg && T >= 2 && T <= pdl::kSegMaxRows && (stride == 1 || (R == 1 && S == 1 && pad == 0))) {
+            const long long bands = (long long)((N + gi - 1) / gi) * g.P;
+            const long long mt = (bands + T - 1) / T;
+            // only when it removes whole waves of the persistent grid: within one wave the
+            // per-tile latency is what counts, and a tile spanning images issues 2-3 boxes
+            // per k-block (measured 2-6% slower at 32-64 images when the wave count is unchanged)
+            const long long wave = sm_count;
+            const long long w_box = ((long long)g.m_tiles * n_tiles + wave - 1) / wave;
+            const long long w_seg = (mt * n_tiles + wave - 1) / wave;
+            if ((w_seg < w_box || (force_seg && mt < g.m_tiles)) && mt < (1ll << 30)) {
+                g.seg_mode = 1;
+                g.seg_tile = T;
+                g.seg_imgs = gi;
+                g.m_tiles = (int)mt;
+                g.flat = false;
+                g.Hg = H;
+                g.Wg = W;
+                g.Pg = g.P;
+                g.Qg = g.Q;
+                g.BW = band;  // epilogue / transaction bytes: T bands of `band` pixels
+                g.BH = T;
+                g.BNI = 1;
+            }
         }
     }
     return g;
@@ -605,11 +609,11 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         const cuuint64_t cs = stride == 1 ? 64 : 128, rs = stride == 1 ? (cuuint64_t)W * 64 : (cuuint64_t)W * 128;
         const cuuint64_t dims[5] = {16, (cuuint64_t)Wv, (cuuint64_t)Hv, (cuuint64_t)CT, (cuuint64_t)N};
         const cuuint64_t str[4] = {cs, rs, (cuuint64_t)H * W * 64, (cuuint64_t)CT * H * W * 64};
-        for (int h = 1; h <= g.seg_tile; ++h) {
-            const cuuint32_t box[5] = {16, (cuuint32_t)g.Q, (cuuint32_t)h, 1, 1};
+        for (int h = 1; h <= std::min(g.seg_tile, g.P); ++h) {
+            const cuuint32_t box[5] = {16, (cuuint32_t)g.Q, (cuuint32_t)h, 1, (cuuint32_t)g.seg_imgs};
             if ((rc = encode(&maps.a[h - 1], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B, "conv x rows")))
                 return rc;
-            if ((rc = encode_y(&maps.y[h - 1], y, N, KT, g.P, g.Q, g.Q, h, 1))) return rc;
+            if ((rc = encode_y(&maps.y[h - 1], y, N, KT, g.P, g.Q, g.Q, h, g.seg_imgs))) return rc;
         }
     } else if (stride == 1) {
         const cuuint64_t dims[5] = {16, (cuuint64_t)g.Wg, (cuuint64_t)g.Hg, (cuuint64_t)CT, (cuuint64_t)N};
@@ -678,7 +682,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.tiles_h = g.tiles_h;
     p.seg_mode = g.seg_mode;
     p.seg_tile = g.seg_tile;
-    p.seg_bytes = g.Q * 64;
+    p.seg_bytes = g.Q * g.seg_imgs * 64;
+    p.seg_imgs = g.seg_imgs;
     p.m_tiles = m_tiles;
     p.raster = cfg.raster;
     p.n_tiles = n_tiles;

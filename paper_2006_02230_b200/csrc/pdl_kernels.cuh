@@ -59,11 +59,13 @@ struct TileParams {
     int box_w, box_h;      // stem: halo tile (input pixels x input rows) of one output tile
     int halo_odd;          // packed stride-2 stem: byte offset of the odd-column halo region
                            // (0: one contiguous halo box)
-    // segment tiles (conv, small even-width maps): an M tile is seg_tile consecutive output
-    // rows of the (image, row) sequence -- the end of one image and the start of the next --
-    // loaded as two exact-height boxes stacked at a 128-byte-aligned smem offset (TMA swizzles
-    // by absolute smem address, so the stack is the canonical SW64 tile).  0: box tiles.
-    int seg_mode, seg_tile, seg_bytes;
+    // segment tiles (conv, small maps): an M tile is seg_tile consecutive "bands" of the
+    // (image group, output row) sequence -- a band is one output row of seg_imgs images
+    // (1 for even Q, 2 for odd Q, so a band is a multiple of 128 bytes) -- loaded as up to
+    // three exact-height boxes {Q, h rows, seg_imgs images} stacked at 128-byte-aligned smem
+    // offsets (TMA swizzles by absolute smem address, so the stack is the canonical SW64
+    // tile; the epilogue stores the same boxes).  seg_mode 0: box tiles.
+    int seg_mode, seg_tile, seg_bytes, seg_imgs;
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
@@ -321,7 +323,7 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     if (KIND == KIND_GEMM) {
         c.m0 = mt * 128;
     } else if (p.seg_mode) {
-        // segment tiles: output rows [mt * seg_tile, +seg_tile) of the (image, row) sequence
+        // segment tiles: bands [mt * seg_tile, +seg_tile); i0 = image group, p0 = first row
         const int g0 = mt * p.seg_tile;
         c.i0 = g0 / p.P;
         c.p0 = g0 - c.i0 * p.P;
@@ -543,15 +545,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         if (p.flags & DBG_NO_A_TMA) {
                         } else if (p.seg_mode) {
-                            // rows p0.. of image i0 (h1 rows), then rows 0.. of image i0 + 1
-                            const int h1 = min(p.seg_tile, p.P - tc.p0), h2 = p.seg_tile - h1;
+                            // bands p0.. of image group i0, then the next group(s) from row 0
+                            int grp = tc.i0, r = tc.p0, left = p.seg_tile, off = 0;
+                            while (left > 0) {
+                                const int h = min(left, p.P - r);
 #pragma unroll
-                            for (int c = 0; c < CG; ++c) {
-                                uint8_t *dst = sp + L::A_OFF + c * G::A_SUB;
-                                tma_load_5d(dst, &maps.a[h1 - 1], &full[s], 0, dw, tc.p0 + dh, ctg * CG + c, tc.i0);
-                                if (h2)
-                                    tma_load_5d(dst + h1 * p.seg_bytes, &maps.a[h2 - 1], &full[s], 0, dw, dh,
-                                                ctg * CG + c, tc.i0 + 1);
+                                for (int c = 0; c < CG; ++c)
+                                    tma_load_5d(sp + L::A_OFF + c * G::A_SUB + off, &maps.a[h - 1], &full[s], 0,
+                                                dw, r + dh, ctg * CG + c, grp * p.seg_imgs);
+                                off += h * p.seg_bytes;
+                                left -= h;
+                                ++grp;
+                                r = 0;
                             }
                         } else {
 #pragma unroll
@@ -1004,11 +1009,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (leader) {
                         if (col0 >= p.n_out || (p.flags & DBG_NO_EPI_STORE)) {
                         } else if (p.seg_mode) {
-                            const int h1 = min(p.seg_tile, p.P - tc.p0), h2 = p.seg_tile - h1;
-                            tma_store_5d(&maps.y[h1 - 1], ebuf, 0, 0, tc.p0, col0 >> 4, tc.i0);
-                            if (h2)
-                                tma_store_5d(&maps.y[h2 - 1], ebuf + h1 * p.seg_bytes, 0, 0, 0, col0 >> 4,
-                                             tc.i0 + 1);
+                            int grp = tc.i0, r = tc.p0, left = p.seg_tile;
+                            uint32_t off = 0;
+                            while (left > 0) {
+                                const int h = min(left, p.P - r);
+                                tma_store_5d(&maps.y[h - 1], ebuf + off, 0, 0, r, col0 >> 4, grp * p.seg_imgs);
+                                off += (uint32_t)(h * p.seg_bytes);
+                                left -= h;
+                                ++grp;
+                                r = 0;
+                            }
                         } else {
                             tma_store_5d(&maps.y[0], ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
                         }

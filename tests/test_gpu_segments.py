@@ -1,7 +1,8 @@
-"""Segment tiles: for small even-width output maps (14x14) an M tile is the next
-128/Q output rows of the (image, row) sequence, loaded as two exact-height boxes
-(end of one image, start of the next) stacked at a 128-byte-aligned smem offset,
-so tiles span images and fill 126 of 128 rows instead of 98 on average.  The TMA swizzle follows absolute shared-memory address bits
+"""Segment tiles: for small output maps (14x14, 7x7) an M tile is the next T
+"bands" of the (image group, output row) sequence -- a band is one output row of
+one image (even Q) or of two images (odd Q) -- loaded as up to three exact-height
+boxes stacked at 128-byte-aligned smem offsets, so tiles span images and fill
+126 of 128 rows instead of 98 on average.  The TMA swizzle follows absolute shared-memory address bits
 (scripts/tma_swizzle_probe.cu), so the stack is the canonical SW64 tile.  Checked
 against the fp64 oracle and bitwise against box tiles (same per-element reduction
 order), for stride 1 / 2, 1x1 / 3x3, odd batches, TF32 and split-K."""
@@ -33,9 +34,9 @@ CASES = [  # (C, K, H, R, stride, N)
     (256, 256, 14, 3, 1, 3),    # 14x14 3x3 (layer 12 shape), one row per segment
     (256, 128, 14, 1, 1, 5),    # 14x14 1x1 (layer 13/15 shape, otherwise flattened)
     (512, 256, 28, 1, 2, 3),    # 28 -> 14 stride 2 (layer 11 / 14 shape)
-    (512, 128, 7, 3, 1, 3),     # 7x7 3x3 (layer 17 shape): odd width, stays on box tiles
-    (256, 256, 7, 1, 1, 4),     # 7x7 1x1 (layer 18 / 20 shape)
-    (256, 128, 14, 1, 2, 5),    # 14 -> 7 stride 2 (layer 16 / 19 shape)
+    (512, 128, 7, 3, 1, 9),     # 7x7 3x3 (layer 17 shape): two-image bands, odd N
+    (256, 256, 7, 1, 1, 10),    # 7x7 1x1 (layer 18 / 20 shape): up to three boxes per tile
+    (256, 128, 14, 1, 2, 9),    # 14 -> 7 stride 2 (layer 16 / 19 shape)
     (64, 32, 16, 3, 1, 3),      # 16x16: 8 rows per tile, whole tiles inside images
     (32, 48, 12, 3, 1, 5),      # 12x12: 10 rows per tile (the most row counts)
 ]
