@@ -401,8 +401,10 @@ def run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream):
 
     def step():
         for (layer, x, w, b, pw, y), xh, yh in zip(bufs, hx, hy):
+            # every layer's input is a host array prepared before the step (x_ready):
+            # a layer's copies in overlap the previous layer's copies out
             P.conv2d_nchw16c_host(xh, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
-                                  mode=args.mode, out=yh)
+                                  mode=args.mode, out=yh, x_ready=True)
 
     steps = max(1, min(args.steps, 3))
     step()

@@ -74,7 +74,10 @@ enum {
     PDL_MODE_3XTF32 = 0 << 4, /* default                                       */
     PDL_MODE_TF32 = 1 << 4,
     PDL_MODE_FP32 = 2 << 4,
-    PDL_MODE_MASK = 3 << 4
+    PDL_MODE_MASK = 3 << 4,
+    PDL_HOST_X_READY = 1 << 6 /* pdl_conv2d_fwd_host: x_host is final at call time (not
+                                 written by work still pending on the stream), so its
+                                 copies may overlap an earlier call's copies out     */
 };
 
 enum {
@@ -132,9 +135,12 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
  * chunks of `chunk` images (0 = library default, ~16 MB of x per chunk); each
  * chunk's host->device copy, convolution (on `stream`) and device->host copy
  * run on separate streams through 3 staging slots, so both PCIe directions and
- * the tensor cores overlap.  Ordered after prior work on `stream`; work
- * enqueued on `stream` after the call sees y_host complete.  workspace must
- * hold pdl_conv2d_host_workspace_bytes(...) bytes (same chunk). */
+ * the tensor cores overlap.  Ordered after prior work on `stream` (with
+ * PDL_HOST_X_READY in flags only the device side is: the copies in may start
+ * while an earlier call's copies out are still running); work enqueued on
+ * `stream` after the call sees y_host complete.  workspace must hold
+ * pdl_conv2d_host_workspace_bytes(...) bytes (same chunk): an x half written by
+ * copies in and a y half read by copies out. */
 size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R, int S,
                                        int stride, int pad, int chunk);
 int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *bias,

@@ -19,6 +19,7 @@ PDL_MODE_3XTF32 = 0 << 4
 PDL_MODE_TF32 = 1 << 4
 PDL_MODE_FP32 = 2 << 4
 PDL_MODE_MASK = 3 << 4
+PDL_HOST_X_READY = 1 << 6
 PDL_OP_CONV2D = 1
 PDL_OP_GEMM = 2
 

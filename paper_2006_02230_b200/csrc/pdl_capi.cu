@@ -705,6 +705,8 @@ struct HostPipe {
     bool ready = false;
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t entry = nullptr, x_in[kHostSlots], done[kHostSlots], y_out[kHostSlots];
+    cudaEvent_t x_free = nullptr;     // last conv of the previous call (x area no longer read)
+    const void *last_ws = nullptr;    // workspace of the previous call
 };
 thread_local HostPipe g_pipe[kMaxDevices];
 
@@ -717,7 +719,8 @@ int host_pipe(HostPipe **out) {
         const unsigned ef = cudaEventDisableTiming;
         bool ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&hp.entry, ef) == cudaSuccess;
+                  cudaEventCreateWithFlags(&hp.entry, ef) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&hp.x_free, ef) == cudaSuccess;
         for (int i = 0; ok && i < kHostSlots; ++i)
             ok = cudaEventCreateWithFlags(&hp.x_in[i], ef) == cudaSuccess &&
                  cudaEventCreateWithFlags(&hp.done[i], ef) == cudaSuccess &&
@@ -835,7 +838,9 @@ size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R,
     if (P <= 0 || Q <= 0) return 0;
     const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
     const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
-    return (size_t)kHostSlots * (align256(c * x_img) + align256(c * y_img));
+    // [x area | y area], equal halves: copies in only write the x area and copies out
+    // only read the y area, so a call's H2D never waits for an earlier call's D2H
+    return 2 * align256((size_t)kHostSlots * std::max(align256(c * x_img), align256(c * y_img)));
 }
 
 int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *bias,
@@ -867,21 +872,29 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
     const size_t xs = align256(c * x_img), ys = align256(c * y_img);
     uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
+    uint8_t *ws_y = ws + (ws_bytes / 2 & ~(size_t)255);  // y area: second half
     cudaStream_t st = (cudaStream_t)stream;
+    const unsigned cflags = flags & ~(unsigned)PDL_HOST_X_READY;
     // chunk i uses slot i % kHostSlots:
     //   h2d: [slot's previous conv done] copy x  -> x_in
     //   st : [x_in, slot's previous y copy done] conv -> done
     //   d2h: [done] copy y -> y_out
-    // entry orders the first use of every slot after prior work on `stream`.
-    if (cudaEventRecord(hp->entry, st) != cudaSuccess || cudaStreamWaitEvent(hp->h2d, hp->entry, 0) != cudaSuccess)
+    // entry orders the first use of every slot after prior work on `stream`.  With
+    // PDL_HOST_X_READY (x_host is final now) and the workspace of the previous call, the
+    // copies in only wait for that call's convolutions to release the x area, so they
+    // overlap the previous call's copies out (consecutive layers pipeline end to end).
+    if (cudaEventRecord(hp->entry, st) != cudaSuccess)
         return fail(PDL_ELAUNCH, "conv host: entry event");
+    const bool relaxed = (flags & PDL_HOST_X_READY) && hp->last_ws == workspace;
+    if (cudaStreamWaitEvent(hp->h2d, relaxed ? hp->x_free : hp->entry, 0) != cudaSuccess)
+        return fail(PDL_ELAUNCH, "conv host: entry wait");
     const int nchunks = (N + c - 1) / c;
     int launches = 0;
     for (int i = 0; i < nchunks; ++i) {
         const int b = i % kHostSlots;
         const int n0 = i * c, n = std::min(c, N - n0);
-        float *xd = reinterpret_cast<float *>(ws + b * (xs + ys));
-        float *yd = reinterpret_cast<float *>(ws + b * (xs + ys) + xs);
+        float *xd = reinterpret_cast<float *>(ws + b * xs);
+        float *yd = reinterpret_cast<float *>(ws_y + b * ys);
         if (i >= kHostSlots && cudaStreamWaitEvent(hp->h2d, hp->done[b], 0) != cudaSuccess)
             return fail(PDL_ELAUNCH, "conv host: wait");
         if (cudaMemcpyAsync(xd, reinterpret_cast<const uint8_t *>(x_host) + n0 * x_img, n * x_img,
@@ -892,7 +905,7 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
             (i >= kHostSlots && cudaStreamWaitEvent(st, hp->y_out[b], 0) != cudaSuccess))
             return fail(PDL_ELAUNCH, "conv host: wait");
         if ((rc = conv_fwd_tc(xd, reinterpret_cast<const float *>(packed_w), bias, yd, n, C, K, H, W,
-                              R, S, stride, pad, flags, cfg, st)))
+                              R, S, stride, pad, cflags, cfg, st)))
             return rc;
         launches += g_launches;
         if (cudaEventRecord(hp->done[b], st) != cudaSuccess ||
@@ -902,6 +915,9 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
             cudaEventRecord(hp->y_out[b], hp->d2h) != cudaSuccess)
             return fail(PDL_ELAUNCH, "conv host: D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
     }
+    // the x area is free once the last convolution has run (next call's copies in)
+    if (cudaEventRecord(hp->x_free, st) != cudaSuccess) return fail(PDL_ELAUNCH, "conv host: x_free");
+    hp->last_ws = workspace;
     // later work on `stream` (and the next call's slot reuse) sees every y copy done
     for (int b = 0; b < std::min(nchunks, kHostSlots); ++b)
         if (cudaStreamWaitEvent(st, hp->y_out[b], 0) != cudaSuccess)

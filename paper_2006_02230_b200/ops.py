@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (PDL_BIAS, PDL_OP_GEMM, PDL_RELU, MODES, TileCfg, check, lib)
+from ._lib import (PDL_BIAS, PDL_HOST_X_READY, PDL_OP_GEMM, PDL_RELU, MODES, TileCfg, check, lib)
 
 
 def _mode(mode: str) -> int:
@@ -180,13 +180,16 @@ def _host_workspace(device, nbytes: int) -> torch.Tensor:
 def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | None = None,
                         stride: int = 1, pad: int = 0, relu: bool = False, mode: str = "3xtf32",
                         cfg=None, out: torch.Tensor | None = None, chunk: int = 0,
-                        device=None, stream=None) -> torch.Tensor:
+                        device=None, stream=None, x_ready: bool = False) -> torch.Tensor:
     """Blocked conv fwd over HOST buffers (the reference's interpret() contract:
     host arrays in, host array out).  x / out are CPU float32 tensors -- pinned
     for full PCIe speed -- weights (PackedWeights) and bias live on the GPU.  The
     library pipelines image chunks: H2D copy, fused conv and D2H copy overlap
     (pdl_conv2d_fwd_host).  Returns `out` (allocated pinned if None), complete
-    once `stream` reaches the point after this call."""
+    once `stream` reaches the point after this call.  x_ready=True promises that
+    x is not written by work still pending on `stream` (e.g. it is not the output
+    of an earlier host call): its copies in may then overlap the previous call's
+    copies out (PDL_HOST_X_READY)."""
     if not isinstance(w, PackedWeights):
         raise TypeError("conv2d_nchw16c_host takes PackedWeights (prepack_weights())")
     if not isinstance(x, torch.Tensor) or x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
@@ -207,6 +210,8 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     need = lib().pdl_conv2d_host_workspace_bytes(n, w.C, w.K, h, wd, w.R, w.S, stride, pad, chunk)
     ws = _host_workspace(dev, need)
     flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    if x_ready:
+        flags |= PDL_HOST_X_READY
     check(lib().pdl_conv2d_fwd_host(_ptr(x), _ptr(w.data), _ptr(bias), _ptr(y), n, w.C, w.K, h, wd,
                                     w.R, w.S, stride, pad, flags, _cfg_ptr(cfg), int(chunk),
                                     _ptr(ws), ws.numel() * 4, ctypes.c_void_p(_stream(stream))))

@@ -77,3 +77,42 @@ def test_host_pipeline_rejects_bad_arguments(P):
                               out=torch.empty((2, 1, 8, 7, 16)))
     with pytest.raises(P.PdlError):
         P.conv2d_nchw16c_host(torch.from_numpy(x), pw, None, pad=1, chunk=-1)
+
+
+def test_host_calls_overlap_across_layers(P):
+    """x_ready=True: consecutive calls with different layer shapes share the staging
+    workspace while an earlier call's copies out may still run; every output must
+    equal the device call (x and y halves of the workspace never alias)."""
+    layers = [W.ConvLayer(0, 64, 128, 14, 3, 1), W.ConvLayer(0, 128, 64, 28, 1, 2),
+              W.ConvLayer(0, 3, 64, 40, 7, 2), W.ConvLayer(0, 64, 256, 9, 1, 1)]
+    outs, refs = [], []
+    for i, layer in enumerate(layers):
+        x, w, b = W.conv_inputs(layer, 6, seed=30 + i)
+        pw = P.prepack_weights(torch.from_numpy(w).cuda(), channels=layer.C)
+        bd = torch.from_numpy(b).cuda()
+        refs.append(P.conv2d_nchw16c(torch.from_numpy(x).cuda(), pw, bd, stride=layer.stride,
+                                     pad=layer.pad, relu=True, cfg={"split_k": 1}).cpu())
+        outs.append((torch.from_numpy(x).pin_memory(), pw, bd, layer))
+    torch.cuda.synchronize()
+    ys = [P.conv2d_nchw16c_host(xh, pw, bd, stride=l.stride, pad=l.pad, relu=True, chunk=2,
+                                x_ready=True) for xh, pw, bd, l in outs * 2]
+    torch.cuda.synchronize()
+    for i, y in enumerate(ys):
+        assert torch.equal(y, refs[i % len(refs)])
+
+
+def test_host_chained_layers_keep_stream_order(P):
+    """Without x_ready, a call whose x_host is the previous call's y_host waits for
+    those copies out (the reference's chained nests)."""
+    l1 = W.ConvLayer(0, 32, 32, 12, 3, 1)
+    x, w1, b1 = W.conv_inputs(l1, 4, seed=40)
+    _, w2, b2 = W.conv_inputs(l1, 4, seed=41)
+    pw1 = P.prepack_weights(torch.from_numpy(w1).cuda())
+    pw2 = P.prepack_weights(torch.from_numpy(w2).cuda())
+    bd1, bd2 = torch.from_numpy(b1).cuda(), torch.from_numpy(b2).cuda()
+    y1 = P.conv2d_nchw16c_host(torch.from_numpy(x).pin_memory(), pw1, bd1, pad=1, relu=True, chunk=1)
+    y2 = P.conv2d_nchw16c_host(y1, pw2, bd2, pad=1, relu=True, chunk=1)
+    torch.cuda.synchronize()
+    d1 = P.conv2d_nchw16c(torch.from_numpy(x).cuda(), pw1, bd1, pad=1, relu=True, cfg={"split_k": 1})
+    d2 = P.conv2d_nchw16c(d1, pw2, bd2, pad=1, relu=True, cfg={"split_k": 1})
+    assert torch.equal(y2, d2.cpu())
