@@ -100,7 +100,11 @@ const bool g_pdl = [] {
 // Reduction elements accumulated in TMEM before an fp32 round-to-nearest drain.
 constexpr int kSegElems = 256;
 // CTAs per cluster sharing (multicasting) each weight tile.
-constexpr int kDefaultCluster = 2;
+constexpr int kDefaultCluster = 2;      // GEMM: CTAs per cluster sharing (multicasting) B
+// conv: no weight multicast by default.  Round 1i A/B on one box (256 images, CUDA-graph
+// suite): cluster 1 beats cluster 2 on layers 3/7/9/10 (-9/-4/-6/-3%) and ties elsewhere,
+// suite +1.5% (profiles/cluster_ab_r1i.json)
+constexpr int kDefaultConvCluster = 1;
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -346,6 +350,10 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool 
     // to three exact-height boxes {Q, h, images}, so tiles span images and fill T bands of
     // up to 128 pixels.  Only the parity-0 map is used (stride 1, or 1x1 / pad 0 stride 2),
     // and T <= kSegMaxRows box heights.
+    // Odd widths (two-image bands, 7x7) are implemented but only used when forced
+    // (PDL_RASTER_SEG_TILES): on ResNet's 7x7 layers they tie box tiles at best and lose
+    // 9-13% on layers 18/19 (many short tiles: 2-3 boxes per load and store).
+    if (g.Q % 2 && !force_seg) allow_seg = false;
     {
         const int gi = (g.Q % 2) ? 2 : 1;     // images per band
         const int band = gi * g.Q;            // pixels per band
@@ -408,7 +416,7 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c) {
     if (c->bn == 64 && R * S > 1 && CT % 4 == 0) cg = 4;
     c->bk = 16 * cg;
     c->stages = 0;
-    c->cluster_m = kDefaultCluster;
+    c->cluster_m = kDefaultConvCluster;
     c->cluster_n = c->split_k = 1;
     c->raster = 0;
 }
