@@ -117,8 +117,9 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
  * last CTA of a tile sums them in range order (deterministic, independent of
  * arrival order) and runs the fused epilogue.  The workspace (256-byte aligned,
  * pdl_conv2d_splitk_workspace_bytes(...) bytes, 0 = this shape does not split)
- * must be ZERO before its first use; its tile counters reset themselves, so it
- * can be reused by later calls on the same stream (not by concurrent streams). */
+ * starts with a fixed 1 KB block of tile counters that must be ZERO before its
+ * first use; the counters reset themselves, so one workspace can serve later
+ * calls of any shape on the same stream (not concurrent streams). */
 size_t pdl_conv2d_splitk_workspace_bytes(int N, int C, int K, int H, int W, int R, int S,
                                          int stride, int pad, unsigned flags,
                                          const pdl_tile_cfg *cfg);

@@ -100,7 +100,6 @@ const bool g_pdl = [] {
 // Reduction elements accumulated in TMEM before an fp32 round-to-nearest drain.
 constexpr int kSegElems = 256;
 // CTAs per cluster sharing (multicasting) each weight tile.
-constexpr int kDefaultCluster = 2;      // GEMM: CTAs per cluster sharing (multicasting) B
 // conv: no weight multicast by default.  Round 1i A/B on one box (256 images, CUDA-graph
 // suite): cluster 1 beats cluster 2 on layers 3/7/9/10 (-9/-4/-6/-3%) and ties elsewhere,
 // suite +1.5% (profiles/cluster_ab_r1i.json)
@@ -230,8 +229,12 @@ size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 // Split-K plan: when a layer's tiles leave persistent CTAs idle (small per-GPU
 // batches: 7x7 maps at 32 images fill 64 of 148 SMs), each tile's reduction is
 // cut into `split` ranges run as separate units; partials meet in the workspace
-// [ctr: tiles ints][part: tiles x split x 128 x BN fp32].  req: cfg->split_k
-// (0 = auto, 1 = off, > 1 = forced).
+// [ctr: kSplitMaxTiles ints][part: tiles x split x 128 x BN fp32].  The counter
+// block has a FIXED size so that the partials of one plan never land on the
+// counters of another (a workspace reused across shapes keeps zero counters).
+// req: cfg->split_k (0 = auto, 1 = off, > 1 = forced).
+constexpr int kSplitMaxTiles = 256;
+constexpr size_t kSplitCtrBytes = kSplitMaxTiles * sizeof(int);
 struct SplitPlan {
     int split = 1, kb_per = 0;
     size_t bytes = 0;
@@ -254,7 +257,7 @@ SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int s
         double best = 0.85 * (double)((tiles + sm_count - 1) / sm_count) * (num_kb + kOverheadKb);
         for (int s = 2; s <= 16; ++s) {
             const int kps = (num_kb + s - 1) / s;
-            if (kps < 8) break;
+            if (kps < 16) break;  // shorter ranges lose to the partial exchange (512^3 GEMM)
             const double c = (double)((tiles * s + sm_count - 1) / sm_count) * (kps + kOverheadKb) + 0.25 * s;
             if (c < best - 1e-9) {
                 best = c;
@@ -262,6 +265,7 @@ SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int s
             }
         }
     }
+    if (tiles > kSplitMaxTiles) S = 1;  // only small grids split (auto: tiles < #SMs)
     if (S > 1) {
         int kps = (num_kb + S - 1) / S;
         if (kps > seg_kb) {  // ranges on segment edges, unless that unbalances the last range
@@ -272,7 +276,7 @@ SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int s
         if (split > 1) {
             sp.split = split;
             sp.kb_per = kps;
-            sp.bytes = align256((size_t)tiles * sizeof(int)) + (size_t)tiles * split * 128 * bn * sizeof(float);
+            sp.bytes = kSplitCtrBytes + (size_t)tiles * split * 128 * bn * sizeof(float);
         }
     }
     return sp;
@@ -286,17 +290,21 @@ int bind_split(pdl::TileParams &p, const SplitPlan &sp, void *ws, size_t ws_byte
     if (!ws || ws_bytes < sp.bytes)
         return fail(PDL_EWORKSPACE, "split-K x%d needs a zero-initialised workspace of %zu bytes", sp.split, sp.bytes);
     if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(PDL_EALIGN, "split-K workspace must be 256-byte aligned");
-    const int tiles = (p.m_tiles + cl - 1) / cl * cl * p.n_tiles;
     p.ctr = reinterpret_cast<int *>(ws);
-    p.part = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + align256((size_t)tiles * sizeof(int)));
+    p.part = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + kSplitCtrBytes);
     return PDL_OK;
 }
 
 // GEMM tile choice (shared by the launch and the workspace query).
-void gemm_cfg(int N, const pdl_tile_cfg *cfg_in, int *bn, int *cl, int *raster) {
-    *bn = N <= 64 ? 64 : 128;
+void gemm_cfg(int M, int N, const pdl_tile_cfg *cfg_in, int *bn, int *cl, int *raster) {
+    // cluster 1 (no B multicast): equal at 4096^3, 3-10% faster below (r1j A/B)
+    // 64-column tiles when 128-column tiles would not fill one wave: small GEMMs are
+    // latency-bound chains per tile, and twice the CTAs halve the chain (graph-replayed
+    // 256^3 / 512^3 / 1024^3: 9.5 / 16.5 / 21.5 -> 7.3 / 11.9 / 16.6 us; 2048^3 keeps 128)
+    const long long tiles128 = (long long)((M + 127) / 128) * ((N + 127) / 128);
+    *bn = (N <= 64 || tiles128 < sm_count) ? 64 : 128;
     *raster = 0;
-    *cl = kDefaultCluster;
+    *cl = 1;
     if (cfg_in) {
         if (cfg_in->bn) *bn = cfg_in->bn;
         if (cfg_in->cluster_m) *cl = cfg_in->cluster_m;
@@ -307,7 +315,7 @@ void gemm_cfg(int N, const pdl_tile_cfg *cfg_in, int *bn, int *cl, int *raster) 
 size_t gemm_split_bytes(int M, int N, int K, unsigned flags, const pdl_tile_cfg *cfg_in) {
     if (M <= 0 || N <= 0 || K <= 0 || (flags & PDL_MODE_MASK) == PDL_MODE_FP32) return 0;
     int bn, cl, raster;
-    gemm_cfg(N, cfg_in, &bn, &cl, &raster);
+    gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
     if (cl != 1 && cl != 2 && cl != 4) return 0;
     return plan_split((M + 127) / 128, (N + bn - 1) / bn, cl, bn, (K + 31) / 32, kSegElems / 32,
                       cfg_in ? cfg_in->split_k : 0).bytes;
@@ -991,7 +999,7 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     }
     if ((rc = get_encode())) return rc;
     int bn, cl, raster;
-    gemm_cfg(N, cfg_in, &bn, &cl, &raster);
+    gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
     if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "gemm: cluster_m must be 1, 2 or 4");
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -1124,11 +1132,13 @@ int pdl_default_cfg(int op, const int *dims, pdl_tile_cfg *cfg) {
     }
     if (op == PDL_OP_GEMM) {
         // dims = {M, N, K}
+        int bn, cl, raster;
+        gemm_cfg(dims[0], dims[1], nullptr, &bn, &cl, &raster);
         cfg->bm = 128;
-        cfg->bn = dims[1] <= 64 ? 64 : 128;
+        cfg->bn = bn;
         cfg->bk = 32;
         cfg->stages = 0;
-        cfg->cluster_m = kDefaultCluster;
+        cfg->cluster_m = cl;
         cfg->cluster_n = cfg->split_k = 1;
         cfg->raster = 0;
         return PDL_OK;

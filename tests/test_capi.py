@@ -54,21 +54,27 @@ def test_workspace_and_packed_bytes():
     dims = (ctypes.c_int * 10)(256, 64, 128, 14, 14, 3, 3, 1, 1, 0)
     assert L.pdl_conv2d_splitk_workspace_bytes(256, 64, 128, 14, 14, 3, 3, 1, 1, 0, None) == 0
     assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 64 * 128 * 9 * 4
-    # 2 images -> 4 tiles of 128 px, 18 k-blocks: split-K x2 (two ranges of 9 k-blocks);
-    # area = 256 B of tile counters + 4 tiles x 2 ranges x 128 x 128 fp32 partials
-    split = 256 + 4 * 2 * 128 * 128 * 4
-    assert L.pdl_conv2d_splitk_workspace_bytes(2, 64, 128, 14, 14, 3, 3, 1, 1, 0, None) == split
-    dims = (ctypes.c_int * 10)(2, 64, 128, 14, 14, 3, 3, 1, 1, 0)
-    assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 64 * 128 * 9 * 4 + split
+    # 2 images of 14x14 (3x3, C=256 -> 72 k-blocks of 32 channels) -> 4 tiles of 128 px:
+    # split-K x4 (ranges of 18 k-blocks); area = 1 KB of tile counters (fixed) + 4 tiles x
+    # 4 ranges x 128 x 128 fp32 partials
+    split = 1024 + 4 * 4 * 128 * 128 * 4
+    assert L.pdl_conv2d_splitk_workspace_bytes(2, 256, 128, 14, 14, 3, 3, 1, 1, 0, None) == split
+    dims = (ctypes.c_int * 10)(2, 256, 128, 14, 14, 3, 3, 1, 1, 0)
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_CONV2D, dims, None) == 2 * 256 * 128 * 9 * 4 + split
+    # ranges shorter than 16 k-blocks never pay: 64 input channels (18 k-blocks) stay whole
+    assert L.pdl_conv2d_splitk_workspace_bytes(2, 64, 128, 14, 14, 3, 3, 1, 1, 0, None) == 0
     # split_k = 1 turns it off; the stem never splits
     off = _lib.TileCfg.make(split_k=1)
-    assert L.pdl_conv2d_splitk_workspace_bytes(2, 64, 128, 14, 14, 3, 3, 1, 1, 0, ctypes.byref(off)) == 0
+    assert L.pdl_conv2d_splitk_workspace_bytes(2, 256, 128, 14, 14, 3, 3, 1, 1, 0, ctypes.byref(off)) == 0
     assert L.pdl_conv2d_splitk_workspace_bytes(1, 3, 64, 224, 224, 7, 7, 2, 3, 0, None) == 0
-    # GEMM: 4096^3 fills the GPU; 1024^3 (64 tiles) splits in two
+    # GEMM: 4096^3 fills the GPU; 1024^3 uses 64-column tiles (128 tiles, one wave) and
+    # does not split; 512 x 512 x 4096 (32 tiles of 128 x 64, 128 k-blocks) splits x4
     g = (ctypes.c_int * 4)(4096, 4096, 4096, 0)
     assert L.pdl_workspace_bytes(_lib.PDL_OP_GEMM, g, None) == 0
     g = (ctypes.c_int * 4)(1024, 1024, 1024, 0)
-    assert L.pdl_workspace_bytes(_lib.PDL_OP_GEMM, g, None) == 256 + 64 * 2 * 128 * 128 * 4
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_GEMM, g, None) == 0
+    g = (ctypes.c_int * 4)(512, 512, 4096, 0)
+    assert L.pdl_workspace_bytes(_lib.PDL_OP_GEMM, g, None) == 1024 + 32 * 4 * 128 * 64 * 4
 
 
 def test_no_gpu_is_a_loud_error():

@@ -86,6 +86,19 @@ def test_raw_weight_call_with_split(P):
     assert rel(y.cpu().numpy(), ref) <= 1e-5
 
 
+def test_workspace_shared_across_shapes(P):
+    """One cached workspace serves split plans of different tile counts in a row:
+    the counters sit in a fixed block, so one plan's partials never become another
+    plan's counters (regression: a 64-column-tile plan after a 128-column one)."""
+    for (m, n, k, bn) in [(1024, 1024, 1024, 128), (1024, 1024, 1024, 64), (512, 512, 4096, 128),
+                          (1024, 1024, 1024, 64), (256, 192, 2048, 64)]:
+        a, bm = W.gemm_inputs(m, n, k, seed=m + bn)
+        for sk in (2, 3):
+            c = P.gemm(torch.from_numpy(a).cuda(), torch.from_numpy(bm).cuda(),
+                       cfg={"split_k": sk, "bn": bn})
+            assert rel(c.cpu().numpy(), oracle.gemm_f64(a, bm)) <= 1e-5, (m, n, k, bn, sk)
+
+
 @pytest.mark.parametrize("mnk", [(1024, 1024, 1024), (512, 512, 512), (256, 192, 2048),
                                  (100, 68, 3000)])
 @pytest.mark.parametrize("split", [0, 3])
