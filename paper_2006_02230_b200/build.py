@@ -48,6 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(4, "-DPDL_TRACE=1")
     if os.environ.get("PDL_EPI_BUFS"):  # experiments: output-box ring depth per epilogue half
         cmd.insert(4, "-DPDL_EPI_BUFS=%d" % int(os.environ["PDL_EPI_BUFS"]))
+    if os.environ.get("PDL_EPI_BUFS_WIDE"):  # ... of the resident-weight 1x1 / stem instances
+        cmd.insert(4, "-DPDL_EPI_BUFS_WIDE=%d" % int(os.environ["PDL_EPI_BUFS_WIDE"]))
     env = dict(os.environ)
     if os.path.exists("/usr/bin/g++"):
         cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
