@@ -696,6 +696,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.BNI = g.BNI;
     p.tiles_w = g.tiles_w;
     p.tiles_h = g.tiles_h;
+    // coalesced LSU epilogue (box tiles only): forced by cfg raster bit 3
+    p.epi_lsu = (!g.seg_mode && cfg_in && (cfg_in->raster & PDL_RASTER_LSU_EPI)) ? 1 : 0;
     p.seg_mode = g.seg_mode;
     p.seg_tile = g.seg_tile;
     p.seg_bytes = g.Q * g.seg_imgs * 64;

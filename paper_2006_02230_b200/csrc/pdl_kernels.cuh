@@ -66,6 +66,10 @@ struct TileParams {
     // offsets (TMA swizzles by absolute smem address, so the stack is the canonical SW64
     // tile; the epilogue stores the same boxes).  seg_mode 0: box tiles.
     int seg_mode, seg_tile, seg_bytes, seg_imgs;
+    // conv epilogue: 0 = TMA box stores; 1 = warp-local smem transpose + coalesced
+    // st.global.v4 (each instruction writes 8 whole 64-byte pixels; no TMA engine, no
+    // bulk-group waits, no 128-thread barriers).  Box tiles only.
+    int epi_lsu;
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
@@ -977,6 +981,61 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sum[j * 16 + q4 * 4 + 2] = t[q4].z; sum[j * 16 + q4 * 4 + 3] = t[q4].w;
                     }
                 }
+            }
+            if (KIND == KIND_CONV && p.epi_lsu) {
+                // ---- coalesced LSU store (bias + ReLU fused): the warp writes its 32 pixels'
+                // 16-channel block into a private 2 KB smem scratch (SW64-style XOR, conflict
+                // free), then lane t stores 16 bytes of pixel 8i + t/4: 512 contiguous bytes
+                // per instruction wherever the pixels are consecutive in y
+                const uint32_t wbuf = smem0 + L::EPI_OFF + (uint32_t)e * 2048;
+                const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
+                const bool relu = p.flags & PDL_RELU;
+                const int per_img = p.BW * p.BH;
+                const size_t plane = (size_t)p.P * p.Q * 16;
+                // output pixel offsets (floats, channel block 0) of the 4 pixels this lane stores
+                long long off[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = quarter * 32 + 8 * i + (lane >> 2);
+                    const int il = r / per_img, rem = r - il * per_img;
+                    const int hl = rem / p.BW, wl = rem - hl * p.BW;
+                    const int img = tc.i0 + il, pp = tc.p0 + hl, qq = tc.q0 + wl;
+                    const bool ok = r < per_img * p.BNI && il < p.BNI && img < p.nimg && pp < p.P && qq < p.Q;
+                    off[i] = ok ? ((long long)img * p.KT * plane + ((size_t)pp * p.Q + qq) * 16 + (lane & 3) * 4) : -1;
+                }
+#pragma unroll
+                for (int j = 0; j < HALF / 16; ++j) {
+                    const int col0 = tc.n0 + half * HALF + j * 16;
+                    if (col0 >= p.n_out) break;
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        float4 r = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
+                                               sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
+                        if (has_bias) {
+                            const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col0 + q4 * 4));
+                            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+                        }
+                        if (relu) {
+                            r.x = (0.f > r.x) ? 0.f : r.x;
+                            r.y = (0.f > r.y) ? 0.f : r.y;
+                            r.z = (0.f > r.z) ? 0.f : r.z;
+                            r.w = (0.f > r.w) ? 0.f : r.w;
+                        }
+                        sts128(wbuf + lane * 64 + ((q4 ^ ((lane >> 1) & 3)) << 4), r);
+                    }
+                    __syncwarp();
+                    float *ycol = p.out + (size_t)(col0 >> 4) * plane;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int px = 8 * i + (lane >> 2), c = lane & 3;
+                        const float4 v = lds128(wbuf + px * 64 + ((c ^ ((px >> 1) & 3)) << 4));
+                        if (off[i] >= 0 && !(p.flags & DBG_NO_EPI_STORE))
+                            *reinterpret_cast<float4 *>(ycol + off[i]) = v;
+                    }
+                    __syncwarp();
+                }
+                if (tr) trace_ev(p, TR_E_STORED, jt);
+                continue;
             }
             if constexpr (KIND != KIND_GEMM) {
                 // ---- store via TMA (bias + ReLU fused): per 16-channel block, the half's
