@@ -512,10 +512,11 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     {
         const int planes = split ? 2 : 1;
         const int nkb = stem_kblocks(C, R, S), cpk = stem_chunks_per_kb(C, R, S);
-        const cuuint64_t dims[5] = {4, (cuuint64_t)K, (cuuint64_t)cpk, (cuuint64_t)nkb, (cuuint64_t)planes};
-        const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)cpk * K * 16,
-                                   (cuuint64_t)nkb * cpk * K * 16};
-        const cuuint32_t box[5] = {4, (cuuint32_t)bn, (cuuint32_t)cpk, (cuuint32_t)nkb, 1};  // resident
+        // [kb][chunk][plane][K][4] (the lo plane of a chunk follows its hi plane)
+        const cuuint64_t dims[5] = {4, (cuuint64_t)K, (cuuint64_t)planes, (cuuint64_t)cpk, (cuuint64_t)nkb};
+        const cuuint64_t str[4] = {16, (cuuint64_t)K * 16, (cuuint64_t)planes * K * 16,
+                                   (cuuint64_t)cpk * planes * K * 16};
+        const cuuint32_t box[5] = {4, (cuuint32_t)bn, (cuuint32_t)planes, (cuuint32_t)cpk, (cuuint32_t)nkb};  // resident
         if ((rc = encode(&maps.b, wp, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem w")))
             return rc;
     }

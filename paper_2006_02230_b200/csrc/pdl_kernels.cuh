@@ -395,6 +395,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW>;
     constexpr bool TS = L::TS;
     constexpr int STAGES = L::STAGES;
+    // fused-B stem (3xTF32, packed): one accumulator of 2*BN columns ([AhBh + AlBh | AhBl]),
+    // so no accumulator double-buffering (the epilogue drains it in ~150 cycles)
+    constexpr bool FUSED = KIND == KIND_STEM && G::STEM_PACKED && SPLIT3;
+    constexpr int PL = SPLIT3 ? 2 : 1;  // stem weight planes, layout [kb][chunk][plane][BN][4]
+    // accumulator buffer / mbarrier parity of TMEM segment g
+    auto acc_buf = [](int g) { return FUSED ? 0 : (g & 1); };
+    auto acc_par = [](int g) { return (uint32_t)(FUSED ? (g & 1) : ((g >> 1) & 1)); };
     constexpr int TSLOTS = L::TSLOTS;
     constexpr int HALF = BN / 2;  // columns per epilogue warp
     extern __shared__ uint8_t smem_raw[];
@@ -492,10 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (KIND == KIND_STEM && blockIdx.x < num_tiles) {  // CL == 1 here
                 // resident weights of this CTA's N-tile: [plane][kb][KS/4 chunks][BN][4]
                 const int n0 = (blockIdx.x % p.n_tiles) * BN;
+                // [kb][chunk][plane][BN][4]: one box covers both planes of every chunk
                 mbar_arrive_expect_tx(wfull, (uint32_t)(L::PLANES * p.num_kb * (G::KS / 4) * BN * 16));
-                for (int pl = 0; pl < L::PLANES; ++pl)
-                    tma_load_5d(smem + L::W_OFF + pl * StemW<BN, CG>::PLANE_BYTES, &maps.b, wfull, 0,
-                                n0, 0, 0, pl);
+                tma_load_5d(smem + L::W_OFF, &maps.b, wfull, 0, n0, 0, 0, 0);
             }
             int s = 0;
             uint32_t ph = 0;
@@ -617,10 +623,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t d_tmem = tmem_base;
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
                     if (in_seg == 0) {  // new segment: wait for its TMEM buffer to be drained
-                        if (PAIR) mbar_wait_cluster(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
-                        else mbar_wait(&tmem_empty[g & 1], ((g >> 1) & 1) ^ 1);
+                        if (PAIR) mbar_wait_cluster(&tmem_empty[acc_buf(g)], acc_par(g) ^ 1);
+                        else mbar_wait(&tmem_empty[acc_buf(g)], acc_par(g) ^ 1);
                         tc_fence_after();
-                        d_tmem = tmem_base + (uint32_t)((g & 1) * BN);
+                        d_tmem = tmem_base + (uint32_t)(acc_buf(g) * BN);
                     }
                     if (lane == 0) trace_ev(p, TR_M_LOOP, kglob);
                     if (PAIR) mbar_wait_cluster(&tready[t], tph);
@@ -651,23 +657,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                             bhi = smem_desc(st + L::B_HI, 16, 8 * G::B_ROW, lay);
                             blo = smem_desc(st + L::B_LO, 16, 8 * G::B_ROW, lay);
                         } else {
-                            // resident no-swizzle K-major weights: 8-row x 16B core matrices;
-                            // 4-value chunks (2j, 2j+1) are BN*16 B apart
-                            const uint32_t w = smem0 + L::W_OFF + (uint32_t)(kb * (G::KS / 4) * BN * 16);
-                            bhi = smem_desc(w, BN * 16, 128, 0);
-                            blo = smem_desc(w + StemW<BN, CG>::PLANE_BYTES, BN * 16, 128, 0);
+                            // resident no-swizzle K-major weights [kb][chunk][plane][BN][4]: 8-row x
+                            // 16B core matrices; 4-value chunks are PL*BN*16 B apart, the lo plane
+                            // of a chunk sits BN*16 B after its hi plane (so [hi | lo] is one
+                            // 2*BN-row operand for the fused MMA)
+                            const uint32_t w = smem0 + L::W_OFF + (uint32_t)(kb * (G::KS / 4) * PL * BN * 16);
+                            bhi = smem_desc(w, PL * BN * 16, 128, 0);
+                            blo = smem_desc(w + BN * 16, PL * BN * 16, 128, 0);
                         }
                         if (p.flags & DBG_NO_MMA) {
                         } else if constexpr (PAIR) {
                             mma_ts_block2<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
                                           G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
                                 d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
-                        } else if constexpr (G::NK == 10) {  // packed stem: 8 + 2 k-steps
-                            mma_ts_block<8, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2), G::boff(3),
-                                         G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
-                                d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
-                            mma_ts_block<2, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2), G::boff(3)>(
-                                d_tmem, a_t + 64, bhi + G::boff(8), blo + G::boff(8), idesc, 1u);
+                        } else if constexpr (FUSED) {  // packed stem, fused B: 8 + 2 k-steps
+                            constexpr uint32_t i2n = idesc_tf32(128, 2 * BN, 0);
+                            constexpr uint32_t SB = 2 * PL * BN;  // 16-byte units per K=8 step
+                            mma_ts_block_fused<8, G::KS, 0, SB, 2 * SB, 3 * SB, 4 * SB, 5 * SB, 6 * SB, 7 * SB>(
+                                d_tmem, a_t, bhi, i2n, idesc, in_seg != 0);
+                            mma_ts_block_fused<2, G::KS, 0, SB>(d_tmem, a_t + 64, bhi + 8 * SB, i2n, idesc, 1u);
+                        } else if constexpr (KIND == KIND_STEM) {
+                            constexpr uint32_t SB = 2 * PL * BN;  // 16-byte units per K=8 step
+                            if constexpr (G::NK == 10) {  // packed stem: 8 + 2 k-steps
+                                mma_ts_block<8, SPLIT3, G::KS, 0, SB, 2 * SB, 3 * SB, 4 * SB, 5 * SB, 6 * SB, 7 * SB>(
+                                    d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
+                                mma_ts_block<2, SPLIT3, G::KS, 0, SB, 0, 0>(d_tmem, a_t + 64, bhi + 8 * SB,
+                                                                            blo + 8 * SB, idesc, 1u);
+                            } else {
+                                mma_ts_block<G::NK, SPLIT3, G::KS, 0, SB, 2 * SB, 3 * SB, 4 * SB, 5 * SB, 6 * SB,
+                                             7 * SB>(d_tmem, a_t, bhi, blo, idesc, in_seg != 0);
+                            }
                         } else {
                             mma_ts_block<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
                                          G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
@@ -716,8 +735,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     if (++t == TSLOTS) { t = 0; tph ^= 1; }
                     if (++in_seg == seg_kb || kb + 1 == kb1) {
-                        if constexpr (PAIR) mma_commit_pair_elect(&tmem_full[g & 1]);
-                        else mma_commit_elect(&tmem_full[g & 1]);
+                        if constexpr (PAIR) mma_commit_pair_elect(&tmem_full[acc_buf(g)]);
+                        else mma_commit_elect(&tmem_full[acc_buf(g)]);
                         in_seg = 0;
                         ++g;
                     }
@@ -909,11 +928,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
             float sum[HALF];
             for (int sg = 0; sg < nseg; ++sg, ++g) {
-                mbar_wait(&tmem_full[g & 1], (g >> 1) & 1);
+                mbar_wait(&tmem_full[acc_buf(g)], acc_par(g));
                 tc_fence_after();
                 if (tr) trace_ev(p, TR_E_FULL, g);
-                const uint32_t base = tmem_base + lane_off + (uint32_t)((g & 1) * BN + half * HALF);
-                if (sg == 0) {
+                const uint32_t base = tmem_base + lane_off + (uint32_t)(acc_buf(g) * BN + half * HALF);
+                if constexpr (FUSED) {
+                    // [AhBh + AlBh | AhBl]: add the two column halves of this segment
+#pragma unroll
+                    for (int j = 0; j < HALF / 16; ++j) {
+                        float v0[16], v1[16];
+                        tmem_ld16_nowait(base + j * 16, v0);
+                        tmem_ld16_nowait(base + BN + j * 16, v1);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            sum[j * 16 + i] = sg == 0 ? v0[i] + v1[i] : sum[j * 16 + i] + (v0[i] + v1[i]);
+                    }
+                } else if (sg == 0) {
                     // first segment: load straight into the sums (all loads in flight, one wait)
 #pragma unroll
                     for (int j = 0; j < HALF / 16; ++j) tmem_ld16_nowait(base + j * 16, &sum[j * 16]);
@@ -930,8 +961,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tc_fence_before();
-                if (PAIR) mbar_arrive_on(&tmem_empty[g & 1], 0);
-                else mbar_arrive(&tmem_empty[g & 1]);
+                if (PAIR) mbar_arrive_on(&tmem_empty[acc_buf(g)], 0);
+                else mbar_arrive(&tmem_empty[acc_buf(g)]);
                 if (tr) trace_ev(p, TR_E_DRAINED, g);
             }
             if (SPL > 1) {
@@ -1290,7 +1321,7 @@ __global__ void prepack_weights_kernel(const float *__restrict__ w, float *__res
     }
 }
 
-// Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[plane][kchunk][k][4]
+// Stem prepack: KCRS16c16k (CT = 1, C_real <= 4) -> packed[kchunk][plane][k][4]
 // (no-swizzle K-major core matrices, 4 reduction values per 16-byte chunk).
 // Unpacked: chunk = r*8 + tap, value = channel (taps >= S and channels >= C_real
 // zero).  Packed (C=3, 7x7): reduction index q = 4kc + j sits in tap-aligned
@@ -1325,8 +1356,11 @@ __global__ void prepack_stem_weights_kernel(const float *__restrict__ w, float *
         }
         float v = 0.f;
         if (ok) v = w[((((size_t)(k >> 4) * R + r) * S + tap) * 16 + c) * 16 + (k & 15)];
-        out[i] = v;
-        if (split) out[i + plane] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        // layout [kchunk][plane][k][4]: the lo plane of a chunk follows its hi plane
+        const int planes = split ? 2 : 1;
+        const size_t o = ((size_t)kc * planes * K + k) * 4 + j;
+        out[o] = v;
+        if (split) out[o + (size_t)K * 4] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     }
 }
 

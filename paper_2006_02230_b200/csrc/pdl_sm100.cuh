@@ -330,6 +330,38 @@ __device__ __forceinline__ void mma_ts_block(uint32_t d, uint32_t a, uint64_t bh
 #undef PDL_LO
 }
 
+// Fused-B 3xTF32 k-block (narrow N): B holds [Bhi | Blo] as 2N rows, so one N=2BN MMA
+// gives Ahi*Bhi (columns 0..BN) and Ahi*Blo (columns BN..2BN), and an N=BN MMA adds
+// Alo*Bhi into columns 0..BN: 2 MMA instructions and 2 TMEM reads of A per K=8 step
+// instead of 3 (the epilogue adds the two column halves).
+#define PDL_TS_FSTEP(J, OFF, FIRSTPRED)                                                 \
+    "add.u32 ah, %1, " #J "*8;\n\t"                                                     \
+    "add.u64 bh, %2, " OFF ";\n\t"                                                      \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %3, " FIRSTPRED ";\n\t"     \
+    "add.u32 al, ah, %6;\n\t"                                                           \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %4, t;\n\t"
+
+template <int NK, uint32_t KS, uint32_t O0, uint32_t O1, uint32_t O2 = 0, uint32_t O3 = 0,
+          uint32_t O4 = 0, uint32_t O5 = 0, uint32_t O6 = 0, uint32_t O7 = 0>
+__device__ __forceinline__ void mma_ts_block_fused(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc2n,
+                                                   uint32_t idescn, uint32_t acc) {
+    static_assert(NK == 2 || NK == 8, "k-steps per block");
+    if constexpr (NK == 2)
+        asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh;\n\t"
+                     "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                     PDL_TS_FSTEP(0, "%7", "p") PDL_TS_FSTEP(1, "%8", "t")
+                     "}" ::"r"(d), "r"(a), "l"(b), "r"(idesc2n), "r"(idescn), "r"(acc), "n"(KS),
+                     "n"(O0), "n"(O1) : "memory");
+    else
+        asm volatile("{\n\t.reg .pred e, p, t;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh;\n\t"
+                     "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"
+                     PDL_TS_FSTEP(0, "%7", "p") PDL_TS_FSTEP(1, "%8", "t") PDL_TS_FSTEP(2, "%9", "t")
+                     PDL_TS_FSTEP(3, "%10", "t") PDL_TS_FSTEP(4, "%11", "t") PDL_TS_FSTEP(5, "%12", "t")
+                     PDL_TS_FSTEP(6, "%13", "t") PDL_TS_FSTEP(7, "%14", "t")
+                     "}" ::"r"(d), "r"(a), "l"(b), "r"(idesc2n), "r"(idescn), "r"(acc), "n"(KS),
+                     "n"(O0), "n"(O1), "n"(O2), "n"(O3), "n"(O4), "n"(O5), "n"(O6), "n"(O7) : "memory");
+}
+
 // ---------------------------------------------------------------- CTA pairs (cta_group::2)
 // The same k-block issue for an M=256 MMA spread over a CTA pair: the leader
 // issues, A comes from both CTAs' TMEM (128 rows each), B from both CTAs' smem
