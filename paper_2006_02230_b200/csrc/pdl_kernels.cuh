@@ -135,6 +135,9 @@ constexpr int kStemHaloBytes = 16384;
 // output-box ring depth for the output-heavy resident-weight 1x1 convs: their epilogue
 // is the bottleneck -- a 16-channel box store takes ~1000 cycles to
 // release its smem (traces: ResNet layers 4/8 spend 4100-4300 cycles per tile storing)
+#ifndef PDL_STEM_WIDE_EPI
+#define PDL_STEM_WIDE_EPI 0
+#endif
 #ifndef PDL_EPI_BUFS_WIDE
 #define PDL_EPI_BUFS_WIDE 4
 #endif  // stem halo tile: box_w * box_h * 16 B
@@ -203,7 +206,8 @@ struct Smem {
     // one drains (one buffer serialised the epilogue on each TMA store's smem read)
     // (only where smem keeps >= 4 stages: with 64 KB weight planes a 4-deep ring leaves
     // 2 stages and layer 5 ran 28% slower; the stem measured no change)
-    static constexpr int EPI_BUFS = (RESW > 0 && RESW <= 32768) ? PDL_EPI_BUFS_WIDE : PDL_EPI_BUFS;
+    static constexpr int EPI_BUFS = ((RESW > 0 && RESW <= 32768) || (KIND == KIND_STEM && PDL_STEM_WIDE_EPI))
+                                        ? PDL_EPI_BUFS_WIDE : PDL_EPI_BUFS;
     static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * EPI_BUFS * 8192;
     // 227 KB opt-in dynamic smem per CTA, minus 2 KB for barriers + base alignment
     static constexpr int BUDGET = 232448 - 2048 - W_BYTES - EPI_BYTES;
