@@ -362,6 +362,10 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool 
     // (PDL_RASTER_SEG_TILES): on ResNet's 7x7 layers they tie box tiles at best and lose
     // 9-13% on layers 18/19 (many short tiles: 2-3 boxes per load and store).
     if (g.Q % 2 && !force_seg) allow_seg = false;
+    // 3x3 layers: the two boxes per tap and k-block cost what the fuller tiles save (ResNet
+    // layer 12: segment 0.326-0.331 ms vs box 0.323 ms, ncu tensor pipe 64% vs 82%); 1x1
+    // layers gain 4-5% (layers 13/14).  Segment tiles only for 1x1 unless forced.
+    if ((R != 1 || S != 1) && !force_seg) allow_seg = false;
     {
         const int gi = (g.Q % 2) ? 2 : 1;     // images per band
         const int band = gi * g.Q;            // pixels per band
