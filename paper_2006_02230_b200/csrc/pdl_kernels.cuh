@@ -3,15 +3,21 @@
 //     blocked convolution (Fig. 9 nest) and the row-major
 //     GEMM (Fig. 1).  TMA stages operand tiles into 64/128B
 //     swizzled shared memory, one elected thread issues tcgen05.mma kind::tf32
-//     with the fp32 accumulator in TMEM, and four epilogue warps drain TMEM
+//     with the fp32 accumulator in TMEM, and eight epilogue warps drain TMEM
 //     through registers, applying the fused bias + ReLU (Alg. 3, PAPER.md:
-//     566-596) before the only store of the output.
+//     566-596) before the only store of the output (TMA box stores).
 //   * 3xTF32: four staging warps copy each landed A row into TMEM as
 //     hi = x (the tensor core truncates to tf32) and lo = x - tf32(x); the MMA
 //     warp issues hi*hi + hi*lo + lo*hi with A read from TMEM.  Conv weights
 //     are split once at prepack; the GEMM's B lo is formed in shared memory.
-//   * stem (C <= 4 real channels, e.g. ResNet's 3->64 7x7/2): one TMA halo row
-//     of 4-channel pixels per kernel row; the staging warps gather the taps.
+//   * stem (C <= 4 real channels, e.g. ResNet's 3->64 7x7/2): the whole input
+//     halo of a 16x8-pixel tile is one stage (even / odd input columns as two
+//     boxes for stride 2); the staging warps gather tap-aligned 16-value chunks;
+//     3xTF32 issues fused-B MMAs (Ahi x [Bhi | Blo] at N=128, Alo x Bhi at N=64).
+//   * persistent work units: (M tile, N tile[, split-K range]); segment tiles
+//     stack 128-byte-aligned row boxes spanning images for small 1x1 maps;
+//     programmatic dependent launch (griddepcontrol) overlaps the prologue with
+//     the previous kernel on the stream.
 //   * simt kernels: exact-fp32 CUDA-core GEMM / conv (PDL_MODE_FP32, and the
 //     GEMM path for leading dimensions TMA cannot describe), the unfused
 //     bias+ReLU pass, and the weight prepack.

@@ -1,0 +1,43 @@
+"""ResNet layer 3 (64 -> 64, 3x3, 56x56) schedules, isolated graph replay at 256 images."""
+import sys
+
+import torch
+
+sys.path.insert(0, '.')
+import paper_2006_02230_b200 as P
+from paper_2006_02230_b200 import workloads as W
+
+for idx in [int(a) for a in (sys.argv[1:] or ["3"])]:
+    l = W.LAYERS[idx - 1]
+    n = 256
+    x = torch.rand((n, l.C_alloc // 16, l.H, l.W, 16), device='cuda')
+    w = torch.rand((l.K // 16, l.C_alloc // 16, l.R, l.S, 16, 16), device='cuda')
+    b = torch.rand(l.K, device='cuda')
+    pw = P.prepack_weights(w, channels=l.C)
+    y = torch.empty((n, l.K // 16, l.P, l.Q, 16), device='cuda')
+    for name, cfg in (("default", None), ("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2}),
+                      ("bk32", {"bk": 32}), ("pair_bk32", {"cluster_n": 2, "bk": 32})):
+        def call():
+            P.conv2d_nchw16c(x, pw, b, stride=l.stride, pad=l.pad, relu=True, out=y, cfg=cfg)
+        try:
+            call()
+        except Exception as e:
+            print(name, "error", e)
+            continue
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(5):
+                    call()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(4):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"{l.name()} {name}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us", flush=True)
