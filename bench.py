@@ -44,6 +44,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--box-tiles", action="store_true", help="A/B: disable segment tiles (PDL_RASTER_BOX_TILES)")
     ap.add_argument("--lsu-epi", action="store_true", help="A/B: coalesced LSU epilogue (PDL_RASTER_LSU_EPI)")
+    ap.add_argument("--no-halo", action="store_true", help="A/B: per-tap A boxes for 3x3 layers (PDL_RASTER_NO_HALO)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay of the step")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
@@ -243,6 +244,8 @@ def run_suite(args, rank, world, local):
         cfg = dict(cfg or {}, raster=2)
     if args.lsu_epi:  # A/B: coalesced LSU epilogue (box-tile layers)
         cfg = dict(cfg or {}, raster=(cfg or {}).get("raster", 0) | 8)
+    if args.no_halo:  # A/B: one A box per tap for 3x3 layers
+        cfg = dict(cfg or {}, raster=(cfg or {}).get("raster", 0) | 16)
     if args.schedule == "ranked":
         from paper_2006_02230_b200 import rank, variants
         cfgs = [variants.emit_launch(rank.choose_variant(l, n_local, args.mode)) for l in layers]

@@ -111,10 +111,10 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // Persistent launch: grid = as many CTAs (clusters of CL) as can be co-resident,
 // capped by the work.  Clusters of 4 cannot use every SM (GPC granularity), so
 // the co-resident count comes from cudaOccupancyMaxActiveClusters.
-template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0, bool HALO = false>
 int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_ctas, cudaStream_t s) {
-    using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR, RESW>;
-    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR, RESW>;
+    using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
+    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR, RESW, HALO>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_ctas = 0;
@@ -196,6 +196,17 @@ int dispatch_resident(int bn, int cg, int plane_bytes, const pdl::TmaMaps &maps,
         if (bn == 64) return launch_tile<pdl::KIND_CONV, 64, 2, true, 1, false, 65536>(maps, p, work, s);
     }
     return fail(PDL_EUNSUPPORTED, "no resident-weight instance for bn=%d cg=%d (%d B)", bn, cg, plane_bytes);
+}
+
+// Halo conv instances (3xTF32, stride 1, R*S > 1, cluster 1): input halo loaded once per
+// channel group, every tap read from it by the staging warps
+int dispatch_halo(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, cudaStream_t s) {
+    const int work = p.m_tiles * p.n_tiles * std::max(1, p.split);
+    if (bn == 64 && cg == 1) return launch_tile<pdl::KIND_CONV, 64, 1, true, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 64 && cg == 2) return launch_tile<pdl::KIND_CONV, 64, 2, true, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 128 && cg == 1) return launch_tile<pdl::KIND_CONV, 128, 1, true, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, true, 1, false, 0, true>(maps, p, work, s);
+    return fail(PDL_EUNSUPPORTED, "no halo instance for bn=%d cg=%d", bn, cg);
 }
 
 // CTA-pair (cta_group::2) conv instances: 3xTF32, cluster of 2
@@ -623,7 +634,19 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
 
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
-    const cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
+    // halo mode (3xTF32, stride 1, spatial filter): one box of the tile's whole input halo
+    // per channel group instead of one box per tap
+    const int halo_w = g.BW + S - 1, halo_h = g.BH + R - 1;
+    // (not with 64-channel k-blocks: two 64 KB halo buffers leave 2 weight stages, and layer 3
+    // ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated)
+    const bool halo = split && !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 && cg <= 2 &&
+                      !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
+                      halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
+    cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
+    if (halo) {
+        abox[1] = (cuuint32_t)halo_w;
+        abox[2] = (cuuint32_t)halo_h;
+    }
     if (g.seg_mode) {
         // one A map and one y map per box height 1..T (parity-0 view for stride 2)
         const int Wv = stride == 1 ? W : (W + 1) / 2, Hv = stride == 1 ? H : (H + 1) / 2;
@@ -711,6 +734,11 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.raster = cfg.raster;
     p.n_tiles = n_tiles;
     if ((rc = bind_split(p, spl, ws, ws_bytes, cl))) return rc;
+    if (halo) {
+        p.box_w = halo_w;
+        p.box_h = halo_h;
+        return dispatch_halo(cfg.bn, cg, maps, p, st);
+    }
     if (pair) return dispatch_pair(cfg.bn, cg, maps, p, st);
     if (resident) {
         p.res_bytes = res_plane;

@@ -193,7 +193,13 @@ struct StemW {
 // SMEM stages (TMA ring) and TMEM A slots (split -> MMA ring) are separate rings.
 // RESW (1x1 conv): the N-tile's whole weight slice stays resident in smem (RESW
 // bytes reserved per plane), loaded once per CTA; stages then carry A only.
-template <int KIND, int BN, int CG, bool SPLIT3, bool PAIR = false, int RESW = 0>
+// HALO (3xTF32 spatial conv, stride 1): the input halo of a tile -- (BW+S-1) x (BH+R-1)
+// pixels of CG 16-channel sub-tiles -- is loaded once per channel group into one of two
+// halo buffers, and the staging warps read every tap's shifted window from it; stages
+// then carry B only (the per-tap A boxes re-read every input pixel R*S times).
+constexpr int kHaloSub = 16384;  // bytes per 16-channel sub-tile of a halo buffer (<= 256 px)
+
+template <int KIND, int BN, int CG, bool SPLIT3, bool PAIR = false, int RESW = 0, bool HALO = false>
 struct Smem {
     using G = Geo<KIND, BN, CG, PAIR>;
     static constexpr bool TS = SPLIT3 || KIND == KIND_STEM;
@@ -205,7 +211,10 @@ struct Smem {
     static constexpr int LOAD_PLANES = KIND == KIND_GEMM ? 1 : PLANES;
     // stem weights stay resident for the whole kernel (one N-tile per CTA)
     static constexpr int W_BYTES = KIND == KIND_STEM ? PLANES * StemW<BN, CG>::PLANE_BYTES : PLANES * RESW;
-    static constexpr int STAGE = (KIND == KIND_STEM || RESW) ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
+    static constexpr int STAGE = HALO ? G::B_BYTES * PLANES
+                                 : (KIND == KIND_STEM || RESW) ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
+    static constexpr int HALO_BUF = CG * kHaloSub;
+    static constexpr int HALO_BYTES = HALO ? 2 * HALO_BUF : 0;
     // conv / stem epilogue: one 128-row x 16-channel (8 KB, SW64) TMA-store buffer
     // per column half of the epilogue warps
     // two output-box buffers per column half: a box is filled while the previous
@@ -216,7 +225,7 @@ struct Smem {
                                         ? PDL_EPI_BUFS_WIDE : PDL_EPI_BUFS;
     static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * EPI_BUFS * 8192;
     // 227 KB opt-in dynamic smem per CTA, minus 2 KB for barriers + base alignment
-    static constexpr int BUDGET = 232448 - 2048 - W_BYTES - EPI_BYTES;
+    static constexpr int BUDGET = 232448 - 2048 - W_BYTES - EPI_BYTES - HALO_BYTES;
     static constexpr int S0 = BUDGET / STAGE;
     static constexpr int STAGES = S0 > 16 ? 16 : S0;
     static constexpr int SLOT_COLS = SPLIT3 ? 2 * G::KS : G::KS;  // TMEM columns per A slot
@@ -224,9 +233,10 @@ struct Smem {
     static constexpr int T0 = TS ? (512 - A_SLOT0) / SLOT_COLS : 1;
     static constexpr int TSLOTS = T0 > 8 ? 8 : T0;
     static constexpr int A_OFF = 0;
-    static constexpr int B_HI = G::A_BYTES;
+    static constexpr int B_HI = HALO ? 0 : G::A_BYTES;
     static constexpr int B_LO = B_HI + G::B_BYTES;
-    static constexpr int W_OFF = STAGES * STAGE;       // stem weights
+    static constexpr int HALO_OFF = STAGES * STAGE;   // halo buffers (HALO)
+    static constexpr int W_OFF = HALO_OFF + HALO_BYTES;  // stem / resident weights
     static constexpr int EPI_OFF = W_OFF + W_BYTES;
     static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
     static constexpr int TOTAL = BAR_OFF + 1024 + 1024;  // barriers + alignment slack
@@ -395,14 +405,15 @@ __device__ __forceinline__ void stem_gather_kb(int c, uint32_t sa, uint32_t row_
     }
 }
 
-template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0, bool HALO = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
     static_assert(CL == 1 || KIND != KIND_STEM, "the stem keeps its weights resident");
     static_assert(!PAIR || (CL == 2 && KIND == KIND_CONV && SPLIT3), "pairs: 3xTF32 conv, cluster 2");
     static_assert(!RESW || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3), "resident weights: 3xTF32 conv");
+    static_assert(!HALO || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3 && !RESW), "halo: 3xTF32 conv");
     using G = Geo<KIND, BN, CG, PAIR>;
-    using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW>;
+    using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
     constexpr bool TS = L::TS;
     constexpr int STAGES = L::STAGES;
     // fused-B stem (3xTF32, packed): one accumulator of 2*BN columns ([AhBh + AlBh | AhBl]),
@@ -424,7 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tmem_full = tfree + 8;       // [2]
     uint64_t *tmem_empty = tmem_full + 2;  // [2]
     uint64_t *wfull = tmem_empty + 2;      // stem weights landed
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
+    uint64_t *hfull = wfull + 1;           // [2] halo buffer landed (HALO)
+    uint64_t *hempty = hfull + 2;          // [2] halo buffer read by every tap (HALO)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(hempty + 2);
     volatile uint32_t *split_flag = tmem_slot + 1;  // split-K: "this CTA reduces the tile"
 
     const int warp = threadIdx.x >> 5;
@@ -458,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // commits of all CL CTAs (B is multicast into every CTA of the cluster)
         // pairs: the leader's one multicast commit per k-block reaches both CTAs;
         // tready / tmem_empty of the leader count both CTAs' staging / epilogue
-        const uint32_t empty_count = (KIND == KIND_STEM || RESW) ? 128 : PAIR ? 129 : (TS ? 128 : 0) + CL;
+        const uint32_t empty_count = HALO ? 1 : (KIND == KIND_STEM || RESW) ? 128 : PAIR ? 129 : (TS ? 128 : 0) + CL;
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], empty_count);
@@ -472,6 +485,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tmem_empty[b], PAIR ? 2 * kEpiThreads : kEpiThreads);
         }
         mbar_init(wfull, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&hfull[b], 1);
+            mbar_init(&hempty[b], 128);
+        }
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -496,9 +513,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t tx;
             if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
             else if (KIND == KIND_CONV)
-                tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
+                tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) || HALO ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
                                 (RESW ? 0 : G::B_BYTES * L::LOAD_PLANES));
             else tx = (uint32_t)(16 * p.box_w * p.box_h * (p.halo_odd ? 2 : 1));
+            // HALO: one box of (box_w x box_h x BNI) pixels per 16-channel sub-tile
+            const uint32_t htx = (uint32_t)(CG * 64 * p.box_w * p.box_h * p.BNI);
+            int hb = 0;
+            uint32_t hph = 0;
             if (RESW && blockIdx.x < num_tiles) {
                 // the grid is a multiple of n_tiles: this CTA keeps one N-tile throughout
                 const int n0 = (blockIdx.x % p.n_tiles) * BN;
@@ -544,6 +565,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kb0 = (u - st * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
                 const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
+                    if constexpr (HALO) {
+                        // new channel group (or the first k-block of this unit): its halo
+                        const int rs_n = p.R * p.S;
+                        const int ctg = kb / rs_n;
+                        if (kb - ctg * rs_n == 0 || kb == kb0) {
+                            mbar_wait(&hempty[hb], hph ^ 1);
+                            mbar_arrive_expect_tx(&hfull[hb], htx);
+                            uint8_t *hbuf = smem + L::HALO_OFF + hb * L::HALO_BUF;
+#pragma unroll
+                            for (int c = 0; c < CG; ++c)
+                                tma_load_5d(hbuf + c * kHaloSub, &maps.a[0], &hfull[hb], 0, tc.q0 - p.pad,
+                                            tc.p0 - p.pad, ctg * CG + c, tc.i0);
+                            if (++hb == 2) { hb = 0; hph ^= 1; }
+                        }
+                    }
                     mbar_wait(&empty[s], ph ^ 1);
                     trace_ev(p, TR_P_ISSUE, kglob);
                     uint8_t *sp = smem + s * L::STAGE;
@@ -571,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             dh = (dh - ph2) >> 1;
                             dw = (dw - pw2) >> 1;
                         }
-                        if (p.flags & DBG_NO_A_TMA) {
+                        if ((p.flags & DBG_NO_A_TMA) || HALO) {
                         } else if (p.seg_mode) {
                             // bands p0.. of image group i0, then the next group(s) from row 0
                             int grp = tc.i0, r = tc.p0, left = p.seg_tile, off = 0;
@@ -856,10 +892,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t ph = 0, tph = 0;
             int kglob = 0;
             const bool tr = tid == 0;
+            // HALO: halo-buffer ring, and this row's halo pixel index at tap (0, 0)
+            int hb = 0;
+            uint32_t hph = 0;
+            int hrow0 = 0;
+            if constexpr (HALO) {
+                const int per_img = p.BW * p.BH;
+                if (row < per_img * p.BNI) {
+                    const int il = row / per_img, rem = row - il * per_img;
+                    const int ph_ = rem / p.BW, pw_ = rem - ph_ * p.BW;
+                    hrow0 = (il * p.box_h + ph_) * p.box_w + pw_;
+                }
+            }
             for (int u = cid; u < num_units; u += ncl) {
                 const int kb0 = (u - (u / SPL) * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
+                    int hrow = 0;
+                    bool group_end = false;
+                    // the stage's B (and A, without HALO) landed: tready below is what the MMA
+                    // warp waits on, so it must imply B is in shared memory
                     mbar_wait(&full[s], ph);
+                    if constexpr (HALO) {
+                        const int rs_n = p.R * p.S;
+                        const int rs = kb - (kb / rs_n) * rs_n;
+                        if (rs == 0 || kb == kb0) mbar_wait(&hfull[hb], hph);
+                        const int r = rs / p.S;
+                        hrow = hrow0 + r * p.box_w + (rs - r * p.S);
+                        group_end = rs == rs_n - 1 || kb + 1 == kb1;
+                    }
                     if (tr) trace_ev(p, TR_S_FULL, kglob);
                     const uint32_t sa = smem0 + s * L::STAGE + L::A_OFF;
                     const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + t * L::SLOT_COLS;
@@ -882,16 +942,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_st32(t_hi + G::KS, lo);
                     } else if (KIND == KIND_CONV) {
                         float x[16 * CG];
+                        if constexpr (HALO) {
+                            // this tap's shifted window of the halo (SW64 by absolute address)
+                            const uint32_t hbuf = smem0 + L::HALO_OFF + hb * L::HALO_BUF + hrow * 64;
 #pragma unroll
-                        for (int c = 0; c < CG; ++c)
+                            for (int c = 0; c < CG; ++c)
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const float4 v =
-                                    lds128(sa + c * G::A_SUB + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
-                                x[16 * c + 4 * j] = v.x; x[16 * c + 4 * j + 1] = v.y;
-                                x[16 * c + 4 * j + 2] = v.z; x[16 * c + 4 * j + 3] = v.w;
+                                for (int j = 0; j < 4; ++j) {
+                                    const float4 v = lds128(hbuf + c * kHaloSub + ((j ^ ((hrow >> 1) & 3)) << 4));
+                                    x[16 * c + 4 * j] = v.x; x[16 * c + 4 * j + 1] = v.y;
+                                    x[16 * c + 4 * j + 2] = v.z; x[16 * c + 4 * j + 3] = v.w;
+                                }
+                            if (group_end) {  // every tap of this channel group has been read
+                                mbar_arrive(&hempty[hb]);
+                                if (++hb == 2) { hb = 0; hph ^= 1; }
                             }
-                        mbar_arrive(&empty[s]);  // A rows read
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < CG; ++c)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const float4 v =
+                                        lds128(sa + c * G::A_SUB + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
+                                    x[16 * c + 4 * j] = v.x; x[16 * c + 4 * j + 1] = v.y;
+                                    x[16 * c + 4 * j + 2] = v.z; x[16 * c + 4 * j + 3] = v.w;
+                                }
+                            mbar_arrive(&empty[s]);  // A rows read
+                        }
                         mbar_wait(&tfree[t], tph ^ 1);
                         if (tr) trace_ev(p, TR_S_TFREE, kglob);
                         tc_fence_after();

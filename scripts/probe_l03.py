@@ -7,7 +7,7 @@ sys.path.insert(0, '.')
 import paper_2006_02230_b200 as P
 from paper_2006_02230_b200 import workloads as W
 
-for idx in [int(a) for a in (sys.argv[1:] or ["3"])]:
+for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     l = W.LAYERS[idx - 1]
     n = 256
     x = torch.rand((n, l.C_alloc // 16, l.H, l.W, 16), device='cuda')
@@ -15,8 +15,12 @@ for idx in [int(a) for a in (sys.argv[1:] or ["3"])]:
     b = torch.rand(l.K, device='cuda')
     pw = P.prepack_weights(w, channels=l.C)
     y = torch.empty((n, l.K // 16, l.P, l.Q, 16), device='cuda')
-    for name, cfg in (("default", None), ("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2}),
-                      ("bk32", {"bk": 32}), ("pair_bk32", {"cluster_n": 2, "bk": 32})):
+    menu = [("default", None), ("no_halo", {"raster": 16})]
+    if "--pairs" in sys.argv:
+        menu += [("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2})]
+    if l.K == 64:
+        menu += [("bk32", {"bk": 32}), ("bk32_no_halo", {"bk": 32, "raster": 16})]
+    for name, cfg in menu:
         def call():
             P.conv2d_nchw16c(x, pw, b, stride=l.stride, pad=l.pad, relu=True, out=y, cfg=cfg)
         try:
