@@ -198,14 +198,17 @@ int dispatch_resident(int bn, int cg, int plane_bytes, const pdl::TmaMaps &maps,
     return fail(PDL_EUNSUPPORTED, "no resident-weight instance for bn=%d cg=%d (%d B)", bn, cg, plane_bytes);
 }
 
-// Halo conv instances (3xTF32, stride 1, R*S > 1, cluster 1): input halo loaded once per
-// channel group, every tap read from it by the staging warps
+// Halo conv instances (stride 1, R*S > 1, cluster 1): input halo loaded once per channel
+// group, every tap read from it by the staging warps (TS MMAs in both modes)
+template <bool SPLIT3>
 int dispatch_halo(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, cudaStream_t s) {
     const int work = p.m_tiles * p.n_tiles * std::max(1, p.split);
-    if (bn == 64 && cg == 1) return launch_tile<pdl::KIND_CONV, 64, 1, true, 1, false, 0, true>(maps, p, work, s);
-    if (bn == 64 && cg == 2) return launch_tile<pdl::KIND_CONV, 64, 2, true, 1, false, 0, true>(maps, p, work, s);
-    if (bn == 128 && cg == 1) return launch_tile<pdl::KIND_CONV, 128, 1, true, 1, false, 0, true>(maps, p, work, s);
-    if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, true, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 64 && cg == 1) return launch_tile<pdl::KIND_CONV, 64, 1, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 64 && cg == 2) return launch_tile<pdl::KIND_CONV, 64, 2, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    if (!SPLIT3 && bn == 64 && cg == 4)
+        return launch_tile<pdl::KIND_CONV, 64, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 128 && cg == 1) return launch_tile<pdl::KIND_CONV, 128, 1, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     return fail(PDL_EUNSUPPORTED, "no halo instance for bn=%d cg=%d", bn, cg);
 }
 
@@ -637,9 +640,11 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // halo mode (3xTF32, stride 1, spatial filter): one box of the tile's whole input halo
     // per channel group instead of one box per tap
     const int halo_w = g.BW + S - 1, halo_h = g.BH + R - 1;
-    // (not with 64-channel k-blocks: two 64 KB halo buffers leave 2 weight stages, and layer 3
-    // ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated)
-    const bool halo = split && !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 && cg <= 2 &&
+    // (3xTF32: not with 64-channel k-blocks -- two 64 KB halo buffers leave 2 weight stages,
+    // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
+    // TF32 stages carry one weight plane, so 64-channel k-blocks keep 4 stages.)
+    const bool halo = !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 &&
+                      (cg <= 2 || (!split && cg == 4)) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
     cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
@@ -737,7 +742,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     if (halo) {
         p.box_w = halo_w;
         p.box_h = halo_h;
-        return dispatch_halo(cfg.bn, cg, maps, p, st);
+        return split ? dispatch_halo<true>(cfg.bn, cg, maps, p, st) : dispatch_halo<false>(cfg.bn, cg, maps, p, st);
     }
     if (pair) return dispatch_pair(cfg.bn, cg, maps, p, st);
     if (resident) {

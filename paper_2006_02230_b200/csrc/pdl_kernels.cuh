@@ -202,7 +202,9 @@ constexpr int kHaloSub = 16384;  // bytes per 16-channel sub-tile of a halo buff
 template <int KIND, int BN, int CG, bool SPLIT3, bool PAIR = false, int RESW = 0, bool HALO = false>
 struct Smem {
     using G = Geo<KIND, BN, CG, PAIR>;
-    static constexpr bool TS = SPLIT3 || KIND == KIND_STEM;
+    // A staged in TMEM (TS MMAs): 3xTF32, the stem, and halo convs (TF32 too: the shifted
+    // tap windows are read by the staging warps, not by the tensor core)
+    static constexpr bool TS = SPLIT3 || KIND == KIND_STEM || HALO;
     static constexpr int PLANES = SPLIT3 ? 2 : 1;  // B planes resident in a stage (hi, lo)
     // B planes loaded by TMA: conv / stem weights carry both (prepacked once); the
     // GEMM loads B itself and the staging warps form lo = B - tf32(B) in smem.
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(CL == 1 || KIND != KIND_STEM, "the stem keeps its weights resident");
     static_assert(!PAIR || (CL == 2 && KIND == KIND_CONV && SPLIT3), "pairs: 3xTF32 conv, cluster 2");
     static_assert(!RESW || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3), "resident weights: 3xTF32 conv");
-    static_assert(!HALO || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3 && !RESW), "halo: 3xTF32 conv");
+    static_assert(!HALO || (KIND == KIND_CONV && CL == 1 && !PAIR && !RESW), "halo: conv, cluster 1");
     using G = Geo<KIND, BN, CG, PAIR>;
     using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
     constexpr bool TS = L::TS;
