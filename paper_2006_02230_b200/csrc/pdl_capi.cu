@@ -647,6 +647,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                       (cg <= 2 || (!split && cg == 4)) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
+    const bool blo_onchip = halo && split && cfg_in && (cfg_in->raster & PDL_RASTER_BLO_ONCHIP);
     cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
     if (halo) {
         abox[1] = (cuuint32_t)halo_w;
@@ -698,6 +699,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         const bool whole = cl == 1 || pair;
         cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(pair ? cfg.bn / 2 : cfg.bn / cl), 1,
                               (cuuint32_t)(whole ? NB : 1), (cuuint32_t)(whole ? planes : 1)};
+        if (blo_onchip) bbox[4] = 1;  // hi plane only
         if (resident) {
             bbox[1] = (cuuint32_t)cfg.bn;
             bbox[3] = (cuuint32_t)(CT * 16 / G);
@@ -740,6 +742,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.n_tiles = n_tiles;
     if ((rc = bind_split(p, spl, ws, ws_bytes, cl))) return rc;
     if (halo) {
+        p.blo_onchip = blo_onchip ? 1 : 0;
         p.box_w = halo_w;
         p.box_h = halo_h;
         return split ? dispatch_halo<true>(cfg.bn, cg, maps, p, st) : dispatch_halo<false>(cfg.bn, cg, maps, p, st);

@@ -76,6 +76,9 @@ struct TileParams {
     // st.global.v4 (each instruction writes 8 whole 64-byte pixels; no TMA engine, no
     // bulk-group waits, no 128-thread barriers).  Box tiles only.
     int epi_lsu;
+    // halo 3xTF32 convs: load only the weights' hi plane; the staging warps form
+    // lo = w - tf32(w) in the stage (halves the weights' TMA fill)
+    int blo_onchip;
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
             else if (KIND == KIND_CONV)
                 tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) || HALO ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
-                                (RESW ? 0 : G::B_BYTES * L::LOAD_PLANES));
+                                (RESW ? 0 : G::B_BYTES * (p.blo_onchip ? 1 : L::LOAD_PLANES)));
             else tx = (uint32_t)(16 * p.box_w * p.box_h * (p.halo_odd ? 2 : 1));
             // HALO: one box of (box_w x box_h x BNI) pixels per 16-channel sub-tile
             const uint32_t htx = (uint32_t)(CG * 64 * p.box_w * p.box_h * p.BNI);
@@ -914,6 +917,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // the stage's B (and A, without HALO) landed: tready below is what the MMA
                     // warp waits on, so it must imply B is in shared memory
                     mbar_wait(&full[s], ph);
+                    if constexpr (HALO && SPLIT3) {
+                        if (p.blo_onchip) {  // weights' lo plane from the landed hi plane
+                            split_lo_smem(smem0 + s * L::STAGE + L::B_HI, smem0 + s * L::STAGE + L::B_LO,
+                                          G::B_BYTES, tid, 128);
+                            fence_proxy_async_smem();  // generic writes -> tensor core (async proxy)
+                        }
+                    }
                     if constexpr (HALO) {
                         const int rs_n = p.R * p.S;
                         const int rs = kb - (kb / rs_n) * rs_n;

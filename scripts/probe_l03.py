@@ -15,7 +15,7 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     b = torch.rand(l.K, device='cuda')
     pw = P.prepack_weights(w, channels=l.C)
     y = torch.empty((n, l.K // 16, l.P, l.Q, 16), device='cuda')
-    menu = [("default", None), ("no_halo", {"raster": 16})]
+    menu = [("default", None), ("no_halo", {"raster": 16}), ("blo_onchip", {"raster": 32})]
     if "--pairs" in sys.argv:
         menu += [("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2})]
     if l.K == 64:
