@@ -70,6 +70,7 @@ typedef struct pdl_tile_cfg {
 #define PDL_RASTER_LSU_EPI 8   /* conv epilogue: coalesced st.global instead of TMA box stores */
 #define PDL_RASTER_NO_HALO 16  /* 3x3 convs: one A box per tap instead of one halo per channel group */
 #define PDL_RASTER_BLO_ONCHIP 32 /* halo 3xTF32 convs: load the weights' hi plane, form lo on chip */
+#define PDL_RASTER_HALO_CG4 64 /* 3xTF32 halo mode with 64-channel k-blocks (one halo buffer) */
 
 enum {
     PDL_BIAS = 1,             /* y += bias[k]                                  */

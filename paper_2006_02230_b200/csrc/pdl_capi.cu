@@ -205,8 +205,7 @@ int dispatch_halo(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParam
     const int work = p.m_tiles * p.n_tiles * std::max(1, p.split);
     if (bn == 64 && cg == 1) return launch_tile<pdl::KIND_CONV, 64, 1, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     if (bn == 64 && cg == 2) return launch_tile<pdl::KIND_CONV, 64, 2, SPLIT3, 1, false, 0, true>(maps, p, work, s);
-    if (!SPLIT3 && bn == 64 && cg == 4)
-        return launch_tile<pdl::KIND_CONV, 64, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 64 && cg == 4) return launch_tile<pdl::KIND_CONV, 64, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     if (bn == 128 && cg == 1) return launch_tile<pdl::KIND_CONV, 128, 1, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     return fail(PDL_EUNSUPPORTED, "no halo instance for bn=%d cg=%d", bn, cg);
@@ -639,12 +638,13 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     std::memset(&maps, 0, sizeof(maps));
     // halo mode (3xTF32, stride 1, spatial filter): one box of the tile's whole input halo
     // per channel group instead of one box per tap
+    const bool halo_cg4 = cfg_in && (cfg_in->raster & PDL_RASTER_HALO_CG4);  // A/B: 3xTF32, 1 halo buffer
     const int halo_w = g.BW + S - 1, halo_h = g.BH + R - 1;
     // (3xTF32: not with 64-channel k-blocks -- two 64 KB halo buffers leave 2 weight stages,
     // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
     // TF32 stages carry one weight plane, so 64-channel k-blocks keep 4 stages.)
     const bool halo = !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 &&
-                      (cg <= 2 || (!split && cg == 4)) &&
+                      (cg <= 2 || (!split && cg == 4) || halo_cg4) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
     const bool blo_onchip = halo && split && cfg_in && (cfg_in->raster & PDL_RASTER_BLO_ONCHIP);

@@ -219,7 +219,10 @@ struct Smem {
     static constexpr int STAGE = HALO ? G::B_BYTES * PLANES
                                  : (KIND == KIND_STEM || RESW) ? G::A_BYTES : G::A_BYTES + G::B_BYTES * PLANES;
     static constexpr int HALO_BUF = CG * kHaloSub;
-    static constexpr int HALO_BYTES = HALO ? 2 * HALO_BUF : 0;
+    // two halo buffers (the next channel group's halo loads during this one's taps), one
+    // for 64-channel k-blocks (two 64 KB buffers would leave two weight stages)
+    static constexpr int HALO_NBUF = CG >= 4 ? 1 : 2;
+    static constexpr int HALO_BYTES = HALO ? HALO_NBUF * HALO_BUF : 0;
     // conv / stem epilogue: one 128-row x 16-channel (8 KB, SW64) TMA-store buffer
     // per column half of the epilogue warps
     // two output-box buffers per column half: a box is filled while the previous
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int c = 0; c < CG; ++c)
                                 tma_load_5d(hbuf + c * kHaloSub, &maps.a[0], &hfull[hb], 0, tc.q0 - p.pad,
                                             tc.p0 - p.pad, ctg * CG + c, tc.i0);
-                            if (++hb == 2) { hb = 0; hph ^= 1; }
+                            if (++hb == L::HALO_NBUF) { hb = 0; hph ^= 1; }
                         }
                     }
                     mbar_wait(&empty[s], ph ^ 1);
@@ -967,7 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             if (group_end) {  // every tap of this channel group has been read
                                 mbar_arrive(&hempty[hb]);
-                                if (++hb == 2) { hb = 0; hph ^= 1; }
+                                if (++hb == L::HALO_NBUF) { hb = 0; hph ^= 1; }
                             }
                         } else {
 #pragma unroll

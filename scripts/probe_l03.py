@@ -19,7 +19,7 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     if "--pairs" in sys.argv:
         menu += [("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2})]
     if l.K == 64:
-        menu += [("bk32", {"bk": 32}), ("bk32_no_halo", {"bk": 32, "raster": 16})]
+        menu += [("halo_cg4", {"raster": 64}), ("bk32", {"bk": 32}), ("bk32_no_halo", {"bk": 32, "raster": 16})]
     for name, cfg in menu:
         def call():
             P.conv2d_nchw16c(x, pw, b, stride=l.stride, pad=l.pad, relu=True, out=y, cfg=cfg)
