@@ -179,6 +179,7 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3, CL>(maps, p, work, s);
         if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3, CL>(maps, p, work, s);
         if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, CL>(maps, p, work, s);
+        if (!SPLIT3 && bn == 128 && cg == 4) return launch_tile<KIND, 128, 4, SPLIT3, CL>(maps, p, work, s);
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
 }
@@ -208,6 +209,9 @@ int dispatch_halo(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParam
     if (bn == 64 && cg == 4) return launch_tile<pdl::KIND_CONV, 64, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     if (bn == 128 && cg == 1) return launch_tile<pdl::KIND_CONV, 128, 1, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    // TF32: 64-channel k-blocks at BN=128 (one halo buffer, one weight plane per stage)
+    if (!SPLIT3 && bn == 128 && cg == 4)
+        return launch_tile<pdl::KIND_CONV, 128, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     return fail(PDL_EUNSUPPORTED, "no halo instance for bn=%d cg=%d", bn, cg);
 }
 
@@ -430,7 +434,7 @@ int stem_chunks_per_kb(int C, int R, int S) { return stem_packed(C, R, S) ? 20 :
 // of 16-channel blocks is even, else 16 (64-byte SW64 rows).
 int weight_group(int C) { return ceil16(C) % 2 == 0 ? 32 : 16; }
 
-void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c) {
+void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flags = 0) {
     const int CT = ceil16(C);
     c->bm = 128;
     c->bn = K >= 128 ? 128 : 64;
@@ -439,6 +443,9 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c) {
     // (the 12 N=64 MMAs of a 32-channel block do not cover the pass overhead;
     // measured 0.39 -> 0.345 ms on ResNet layer 3, profiles/sweep_r1.json)
     if (c->bn == 64 && R * S > 1 && CT % 4 == 0) cg = 4;
+    // TF32 spatial convs at BN=128: 64-channel k-blocks too (one weight plane per stage
+    // leaves room; halo mode: layers 7/12/17 138/148/168 vs 145/153/180 us)
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_TF32 && c->bn == 128 && R * S > 1 && CT % 4 == 0) cg = 4;
     c->bk = 16 * cg;
     c->stages = 0;
     c->cluster_m = kDefaultConvCluster;
@@ -588,7 +595,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     }
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
-    conv_default_cfg(C, K, R, S, &cfg);
+    conv_default_cfg(C, K, R, S, &cfg, flags);
     if (cfg_in) {
         if (cfg_in->bn) cfg.bn = cfg_in->bn;
         if (cfg_in->bk) cfg.bk = cfg_in->bk;
@@ -1170,7 +1177,7 @@ size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg) {
 int pdl_default_cfg(int op, const int *dims, pdl_tile_cfg *cfg) {
     if (!cfg || !dims) return fail(PDL_EINVAL, "default_cfg: null argument");
     if (op == PDL_OP_CONV2D) {
-        conv_default_cfg(dims[1], dims[2], dims[5], dims[6], cfg);
+        conv_default_cfg(dims[1], dims[2], dims[5], dims[6], cfg, (unsigned)dims[9]);
         return PDL_OK;
     }
     if (op == PDL_OP_GEMM) {

@@ -70,7 +70,7 @@ def legal(layer, v: TileVariant) -> bool:
     if _is_stem(layer):
         return v.bn == 64 and v.cluster == 1 and v.bk == 32
     ct = (layer.C + 15) // 16
-    if (v.bn, v.cg) not in _CONV_INSTANCES:
+    if (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
         return False
     if ct % v.cg:
         return False

@@ -13,16 +13,22 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     x = torch.rand((n, l.C_alloc // 16, l.H, l.W, 16), device='cuda')
     w = torch.rand((l.K // 16, l.C_alloc // 16, l.R, l.S, 16, 16), device='cuda')
     b = torch.rand(l.K, device='cuda')
-    pw = P.prepack_weights(w, channels=l.C)
+    mode = "tf32" if "--tf32" in sys.argv else "3xtf32"
+    pw = P.prepack_weights(w, channels=l.C, mode=mode)
     y = torch.empty((n, l.K // 16, l.P, l.Q, 16), device='cuda')
-    menu = [("default", None), ("no_halo", {"raster": 16}), ("blo_onchip", {"raster": 32})]
+    mode = "tf32" if "--tf32" in sys.argv else "3xtf32"
+    menu = [("default", None), ("no_halo", {"raster": 16})]
+    if mode == "tf32" and l.K >= 128:
+        menu += [("bk64", {"bk": 64})]
+    elif mode == "3xtf32":
+        menu += [("blo_onchip", {"raster": 32})]
     if "--pairs" in sys.argv:
         menu += [("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2})]
     if l.K == 64:
         menu += [("halo_cg4", {"raster": 64}), ("bk32", {"bk": 32}), ("bk32_no_halo", {"bk": 32, "raster": 16})]
     for name, cfg in menu:
         def call():
-            P.conv2d_nchw16c(x, pw, b, stride=l.stride, pad=l.pad, relu=True, out=y, cfg=cfg)
+            P.conv2d_nchw16c(x, pw, b, stride=l.stride, pad=l.pad, relu=True, out=y, cfg=cfg, mode=mode)
         try:
             call()
         except Exception as e:

@@ -17,7 +17,7 @@ def test_all_variants_legal(idx, mode):
     assert vs
     from paper_2006_02230_b200 import _lib
     dflt_bk = _lib.default_cfg(_lib.PDL_OP_CONV2D,
-                               [2, L.C, L.K, L.H, L.W, L.R, L.S, L.stride, L.pad, 0]).bk
+                               [2, L.C, L.K, L.H, L.W, L.R, L.S, L.stride, L.pad, _lib.MODES[mode]]).bk
     if L.C <= 4:
         dflt_bk = 32  # the stem ignores bk
     bad = []
