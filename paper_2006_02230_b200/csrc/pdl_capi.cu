@@ -443,9 +443,13 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
     // (the 12 N=64 MMAs of a 32-channel block do not cover the pass overhead;
     // measured 0.39 -> 0.345 ms on ResNet layer 3, profiles/sweep_r1.json)
     if (c->bn == 64 && R * S > 1 && CT % 4 == 0) cg = 4;
-    // TF32 spatial convs at BN=128: 64-channel k-blocks too (one weight plane per stage
-    // leaves room; halo mode: layers 7/12/17 138/148/168 vs 145/153/180 us)
-    if ((flags & PDL_MODE_MASK) == PDL_MODE_TF32 && c->bn == 128 && R * S > 1 && CT % 4 == 0) cg = 4;
+    // TF32: 64-channel k-blocks everywhere the channels allow (one weight plane per stage
+    // leaves room).  A 32-channel TF32 k-block is 4 MMAs against the fixed per-k-block
+    // hand-off; doubling it made the 1x1 layers 25-35% faster (layer 13: 122.8 -> 88.9 us,
+    // layer 19: 207.8 -> 137.8 us) and the halo 3x3 layers 5% faster.
+    // (1x1 layers with <= 128 input channels keep 32-channel blocks: with only 1-2
+    // k-blocks per tile they lose the k-loop pipelining -- layers 2/4/8 were 3-4% slower)
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_TF32 && CT % 4 == 0 && (R * S > 1 || CT >= 16)) cg = 4;
     c->bk = 16 * cg;
     c->stages = 0;
     c->cluster_m = kDefaultConvCluster;

@@ -19,7 +19,7 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     mode = "tf32" if "--tf32" in sys.argv else "3xtf32"
     menu = [("default", None), ("no_halo", {"raster": 16})]
     if mode == "tf32" and l.K >= 128:
-        menu += [("bk64", {"bk": 64})]
+        menu += [("bk64", {"bk": 64}), ("bk32", {"bk": 32})]
     elif mode == "3xtf32":
         menu += [("blo_onchip", {"raster": 32})]
     if "--pairs" in sys.argv:
