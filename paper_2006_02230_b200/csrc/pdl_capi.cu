@@ -179,7 +179,7 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3, CL>(maps, p, work, s);
         if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3, CL>(maps, p, work, s);
         if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, CL>(maps, p, work, s);
-        if (!SPLIT3 && bn == 128 && cg == 4) return launch_tile<KIND, 128, 4, SPLIT3, CL>(maps, p, work, s);
+        if (bn == 128 && cg == 4 && (!SPLIT3 || CL == 1)) return launch_tile<KIND, 128, 4, SPLIT3, CL>(maps, p, work, s);
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
 }
@@ -210,8 +210,7 @@ int dispatch_halo(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParam
     if (bn == 128 && cg == 1) return launch_tile<pdl::KIND_CONV, 128, 1, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     if (bn == 128 && cg == 2) return launch_tile<pdl::KIND_CONV, 128, 2, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     // TF32: 64-channel k-blocks at BN=128 (one halo buffer, one weight plane per stage)
-    if (!SPLIT3 && bn == 128 && cg == 4)
-        return launch_tile<pdl::KIND_CONV, 128, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
+    if (bn == 128 && cg == 4) return launch_tile<pdl::KIND_CONV, 128, 4, SPLIT3, 1, false, 0, true>(maps, p, work, s);
     return fail(PDL_EUNSUPPORTED, "no halo instance for bn=%d cg=%d", bn, cg);
 }
 
@@ -655,7 +654,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
     // TF32 stages carry one weight plane, so 64-channel k-blocks keep 4 stages.)
     const bool halo = !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 &&
-                      (cg <= 2 || (!split && cg == 4) || halo_cg4) &&
+                      (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
     const bool blo_onchip = halo && split && cfg_in && (cfg_in->raster & PDL_RASTER_BLO_ONCHIP);

@@ -20,8 +20,8 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     menu = [("default", None), ("no_halo", {"raster": 16})]
     if mode == "tf32" and l.K >= 128:
         menu += [("bk64", {"bk": 64}), ("bk32", {"bk": 32})]
-    elif mode == "3xtf32":
-        menu += [("blo_onchip", {"raster": 32})]
+    elif mode == "3xtf32" and l.K >= 128:
+        menu += [("bk64", {"bk": 64})]
     if "--pairs" in sys.argv:
         menu += [("pair", {"cluster_n": 2}), ("cl2", {"cluster_m": 2})]
     if l.K == 64:
