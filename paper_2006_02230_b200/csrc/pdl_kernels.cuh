@@ -144,6 +144,9 @@ constexpr int kStemHaloBytes = 16384;
 // output-box ring depth for the output-heavy resident-weight 1x1 convs: their epilogue
 // is the bottleneck -- a 16-channel box store takes ~1000 cycles to
 // release its smem (traces: ResNet layers 4/8 spend 4100-4300 cycles per tile storing)
+#ifndef PDL_BATCH_ALL  // experiments: batched box stores wherever a buffer per box exists
+#define PDL_BATCH_ALL 0
+#endif
 #ifndef PDL_STEM_WIDE_EPI
 #define PDL_STEM_WIDE_EPI 0
 #endif
@@ -229,7 +232,10 @@ struct Smem {
     // one drains (one buffer serialised the epilogue on each TMA store's smem read)
     // (only where smem keeps >= 4 stages: with 64 KB weight planes a 4-deep ring leaves
     // 2 stages and layer 5 ran 28% slower; the stem measured no change)
-    static constexpr int EPI_BUFS = ((RESW > 0 && RESW <= 32768) || (KIND == KIND_STEM && PDL_STEM_WIDE_EPI))
+    static constexpr bool WIDE_FITS =
+        (232448 - 2048 - W_BYTES - HALO_BYTES - 2 * PDL_EPI_BUFS_WIDE * 8192) / STAGE >= 3;
+    static constexpr int EPI_BUFS = ((RESW > 0 && RESW <= 32768) || (KIND == KIND_STEM && PDL_STEM_WIDE_EPI) ||
+                                     (PDL_BATCH_ALL && KIND == KIND_CONV && !RESW && WIDE_FITS))
                                         ? PDL_EPI_BUFS_WIDE : PDL_EPI_BUFS;
     static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * EPI_BUFS * 8192;
     // 227 KB opt-in dynamic smem per CTA, minus 2 KB for barriers + base alignment
@@ -1216,7 +1222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sts128(ebuf + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4), r);
                     }
                 };
-                if constexpr (L::EPI_BUFS >= HALF / 16 && (RESW || KIND == KIND_STEM)) {
+                if constexpr (L::EPI_BUFS >= HALF / 16 && (RESW || KIND == KIND_STEM || PDL_BATCH_ALL)) {
                     // output-heavy tiles with a buffer per box: write every box of the tile,
                     // then store them all (2 barriers per tile instead of 2 per box; stem
                     // -6%, layers 2/4 -5/-11%; compute-bound BN=64 layer 3 keeps the ring)
