@@ -339,9 +339,12 @@ def run_suite(args, rank, world, local):
                     peaks["hbm_gbs"] * 1e9)
     if rf.bound == "tensor":
         achieved = dom_layer.flops(n_local) / dom_s / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
-                "peak_source": peaks["source"] + " bf16 dense",
+        # the kernel is timed inside a multi-millisecond step: the sustained bf16 figure
+        sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": sus,
+                "unit": "TFLOP/s", "frac": round(achieved / sus, 4),
+                "peak_source": peaks["source"] + " bf16 dense, sustained (kernel timed inside the step; "
+                               "burst %.1f)" % peaks["bf16_tflops"],
                 "mode_peak": round(mode_peak / 1e12, 1),
                 "mode_peak_source": f"{peaks['tf32_source']}" + (" / 3 (3xTF32 = 3 tensor passes)" if args.mode == "3xtf32" else ""),
                 "frac_of_mode_peak": round(achieved / (mode_peak / 1e12), 4)}
