@@ -165,11 +165,11 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
 _host_ws: dict = {}
 
 
-def _host_workspace(device, nbytes: int) -> torch.Tensor:
-    """Device staging for conv2d_nchw16c_host, kept per device and grown on demand
-    (every call joins its copy streams back into the caller's stream, so the
-    next call may reuse it)."""
-    key = torch.device(device).index
+def _host_workspace(device, stream_handle: int, nbytes: int) -> torch.Tensor:
+    """Device staging for conv2d_nchw16c_host, kept per (device, stream) and grown
+    on demand: calls on one stream are ordered (each joins its copy streams back
+    into the caller's stream), calls on different streams must not share it."""
+    key = (torch.device(device).index, stream_handle)
     ws = _host_ws.get(key)
     if ws is None or ws.numel() * 4 < nbytes:
         ws = torch.empty((nbytes + 3) // 4, dtype=torch.float32, device=device)
@@ -208,13 +208,14 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
         raise ValueError("out must be a contiguous float32 CPU tensor [N][K/16][P][Q][16]")
     dev = w.data.device if device is None else torch.device(device)
     need = lib().pdl_conv2d_host_workspace_bytes(n, w.C, w.K, h, wd, w.R, w.S, stride, pad, chunk)
-    ws = _host_workspace(dev, need)
+    sh = _stream(stream)
+    ws = _host_workspace(dev, sh, need)
     flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
     if x_ready:
         flags |= PDL_HOST_X_READY
     check(lib().pdl_conv2d_fwd_host(_ptr(x), _ptr(w.data), _ptr(bias), _ptr(y), n, w.C, w.K, h, wd,
                                     w.R, w.S, stride, pad, flags, _cfg_ptr(cfg), int(chunk),
-                                    _ptr(ws), ws.numel() * 4, ctypes.c_void_p(_stream(stream))))
+                                    _ptr(ws), ws.numel() * 4, ctypes.c_void_p(sh)))
     return y
 
 
