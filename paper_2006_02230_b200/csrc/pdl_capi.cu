@@ -180,6 +180,9 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3, CL>(maps, p, work, s);
         if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, CL>(maps, p, work, s);
         if (bn == 128 && cg == 4 && (!SPLIT3 || CL == 1)) return launch_tile<KIND, 128, 4, SPLIT3, CL>(maps, p, work, s);
+        if constexpr (!SPLIT3 && CL == 1) {
+            if (bn == 256 && cg == 2) return launch_tile<KIND, 256, 2, false, 1>(maps, p, work, s);
+        }
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
 }
@@ -433,7 +436,7 @@ int stem_chunks_per_kb(int C, int R, int S) { return stem_packed(C, R, S) ? 20 :
 // of 16-channel blocks is even, else 16 (64-byte SW64 rows).
 int weight_group(int C) { return ceil16(C) % 2 == 0 ? 32 : 16; }
 
-void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flags = 0) {
+void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flags = 0, bool wide = true) {
     const int CT = ceil16(C);
     c->bm = 128;
     c->bn = K >= 128 ? 128 : 64;
@@ -449,6 +452,13 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
     // (1x1 layers with <= 128 input channels keep 32-channel blocks: with only 1-2
     // k-blocks per tile they lose the k-loop pipelining -- layers 2/4/8 were 3-4% slower)
     if ((flags & PDL_MODE_MASK) == PDL_MODE_TF32 && CT % 4 == 0 && (R * S > 1 || CT >= 16)) cg = 4;
+    // TF32 1x1 convs with K >= 256: 256-column tiles (one N=256 MMA per K step, half the A
+    // fill per flop; streaming epilogue), 32-channel k-blocks (48 KB stages)
+    // (not when the caller asks for a multicast cluster or split-K, which 256 tiles lack)
+    if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_TF32 && R == 1 && S == 1 && K % 256 == 0 && CT % 2 == 0) {
+        c->bn = 256;
+        cg = 2;
+    }
     c->bk = 16 * cg;
     c->stages = 0;
     c->cluster_m = kDefaultConvCluster;
@@ -598,7 +608,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     }
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
-    conv_default_cfg(C, K, R, S, &cfg, flags);
+    conv_default_cfg(C, K, R, S, &cfg, flags, !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1)));
     if (cfg_in) {
         if (cfg_in->bn) cfg.bn = cfg_in->bn;
         if (cfg_in->bk) cfg.bk = cfg_in->bk;
@@ -631,10 +641,12 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // layers 12/13/15 at 256 images)
     if (g.seg_mode && !(cfg_in && cfg_in->cluster_m)) cl = 1;
     const int m_tiles = g.m_tiles, n_tiles = (K + cfg.bn - 1) / cfg.bn;
-    const int num_kb = (CT / cg) * R * S, seg_kb = std::max(1, kSegElems / (16 * cg));
+    const int num_kb = (CT / cg) * R * S;
+    // BN=256 (TF32): one accumulation segment per tile, never split (streaming epilogue)
+    const int seg_kb = cfg.bn > 128 ? num_kb : std::max(1, kSegElems / (16 * cg));
     SplitPlan spl;
     spl.kb_per = num_kb;
-    if (!pair && !resident) {
+    if (!pair && !resident && cfg.bn <= 128) {
         const int req = cfg_in ? cfg_in->split_k : 0;
         spl = plan_split(m_tiles, n_tiles, cl, cfg.bn, num_kb, seg_kb, (ws || query) ? req : (req > 1 ? req : 1));
     }

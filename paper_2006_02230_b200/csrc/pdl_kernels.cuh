@@ -426,6 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(!PAIR || (CL == 2 && KIND == KIND_CONV && SPLIT3), "pairs: 3xTF32 conv, cluster 2");
     static_assert(!RESW || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3), "resident weights: 3xTF32 conv");
     static_assert(!HALO || (KIND == KIND_CONV && CL == 1 && !PAIR && !RESW), "halo: conv, cluster 1");
+    static_assert(BN <= 128 || (KIND == KIND_CONV && !SPLIT3 && !HALO && !RESW && CL == 1),
+                  "BN=256: TF32 conv, SS MMAs, cluster 1");
     using G = Geo<KIND, BN, CG, PAIR>;
     using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
     constexpr bool TS = L::TS;
@@ -1034,6 +1036,76 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kb0 = sp * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
             const int nseg = (kb1 - kb0 + seg_kb - 1) / seg_kb;
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
+            if constexpr (KIND == KIND_CONV && BN > 128) {
+                // ---- streaming epilogue (TF32, BN=256: 128 columns per thread do not fit
+                // in registers): one segment per tile (the host sets seg_kb = num_kb, no
+                // split-K); each 16-column block goes TMEM -> registers -> smem box -> TMA
+                // store, and the accumulator is released after its last block is read
+                mbar_wait(&tmem_full[acc_buf(g)], acc_par(g));
+                tc_fence_after();
+                const uint32_t base = tmem_base + lane_off + (uint32_t)(acc_buf(g) * BN + half * HALF);
+                const uint32_t ebase = smem0 + L::EPI_OFF + half * L::EPI_BUFS * 8192;
+                const bool in_box = row < p.BW * p.BH * p.BNI;
+                const bool leader = quarter == 0 && lane == 0;
+                const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
+                const bool relu = p.flags & PDL_RELU;
+#pragma unroll 1
+                for (int j = 0; j < HALF / 16; ++j) {
+                    float v[16];
+                    tmem_ld16_nowait(base + j * 16, v);
+                    tmem_wait_ld();
+                    if (j == HALF / 16 - 1) {
+                        tc_fence_before();
+                        mbar_arrive(&tmem_empty[acc_buf(g)]);
+                    }
+                    const int col0 = tc.n0 + half * HALF + j * 16;
+                    const uint32_t ebuf = ebase + (uint32_t)(eblk % L::EPI_BUFS) * 8192;
+                    ++eblk;
+                    if (leader) bulk_wait_read<L::EPI_BUFS - 1>();
+                    named_bar_sync(2 + half, 128);
+                    if (in_box) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            float4 r = make_float4(v[q4 * 4], v[q4 * 4 + 1], v[q4 * 4 + 2], v[q4 * 4 + 3]);
+                            if (has_bias && col0 < p.n_out) {
+                                const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col0 + q4 * 4));
+                                r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+                            }
+                            if (relu) {
+                                r.x = (0.f > r.x) ? 0.f : r.x;
+                                r.y = (0.f > r.y) ? 0.f : r.y;
+                                r.z = (0.f > r.z) ? 0.f : r.z;
+                                r.w = (0.f > r.w) ? 0.f : r.w;
+                            }
+                            sts128(ebuf + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4), r);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(2 + half, 128);
+                    if (leader) {
+                        if (col0 < p.n_out && !(p.flags & DBG_NO_EPI_STORE)) {
+                            if (p.seg_mode) {
+                                int grp = tc.i0, r = tc.p0, left = p.seg_tile;
+                                uint32_t off = 0;
+                                while (left > 0) {
+                                    const int h = min(left, p.P - r);
+                                    tma_store_5d(&maps.y[h - 1], ebuf + off, 0, 0, r, col0 >> 4, grp * p.seg_imgs);
+                                    off += (uint32_t)(h * p.seg_bytes);
+                                    left -= h;
+                                    ++grp;
+                                    r = 0;
+                                }
+                            } else {
+                                tma_store_5d(&maps.y[0], ebuf, 0, tc.q0, tc.p0, col0 >> 4, tc.i0);
+                            }
+                        }
+                        bulk_commit();
+                    }
+                }
+                ++g;
+                if (tr) trace_ev(p, TR_E_STORED, jt);
+                continue;
+            }
             float sum[HALF];
             for (int sg = 0; sg < nseg; ++sg, ++g) {
                 mbar_wait(&tmem_full[acc_buf(g)], acc_par(g));

@@ -5,7 +5,8 @@ On the CPU a variant is a tiled / interchanged loop nest emitted as C.  On the
 B200 the loop nest is fixed (the persistent tile engine), and what varies is
 the tile configuration a `pdl_tile_cfg` carries:
 
-  bn       output channels (conv K / GEMM N) per CTA tile: 64 | 128
+  bn       output channels (conv K / GEMM N) per CTA tile: 64 | 128 | 256 (TF32 1x1
+           convs only: one accumulation segment per tile, streaming epilogue)
   bk       reduction elements per pipeline stage: 16 * cg, cg in {1, 2, 4}
   cluster  CTAs sharing (multicasting) each weight tile: 1 | 2 | 4
   mode     "3xtf32" | "tf32"
@@ -13,9 +14,10 @@ the tile configuration a `pdl_tile_cfg` carries:
 `generate_variants` enumerates the legal ones deterministically (ids sorted,
 deduplicated), `legality_check` runs a variant against the default schedule on
 the GPU (interpreter-equivalence in the SPEC's sense, at the mode's tolerance:
-variants with the same bk reduce every element in the same order and agree
-bitwise; a different bk re-associates the channel/tap sum inside a 256-element
-accumulation segment), `emit_launch` is the B200 analogue of
+variants with the same bk and segmenting reduce every element in the same order
+and agree bitwise; a different bk re-associates the channel/tap sum inside a
+256-element accumulation segment, and 256-column tiles sum the whole reduction in
+one segment), `emit_launch` is the B200 analogue of
 `emit_c`: the launch configuration (a dict accepted as `cfg=` by the ops).
 `engine_geometry` restates the host's tiling rules (csrc/pdl_capi.cu) so the
 analytical ranker can reason about a variant without launching it.
@@ -45,7 +47,7 @@ class TileVariant:
 
 @dataclass
 class VariantConfig:
-    bn_menu: tuple = (64, 128)
+    bn_menu: tuple = (64, 128, 256)
     cg_menu: tuple = (1, 2, 4)
     cluster_menu: tuple = (1, 2, 4)
     modes: tuple = ("3xtf32",)
@@ -70,7 +72,12 @@ def legal(layer, v: TileVariant) -> bool:
     if _is_stem(layer):
         return v.bn == 64 and v.cluster == 1 and v.bk == 32
     ct = (layer.C + 15) // 16
-    if (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
+    if v.bn == 256:
+        # TF32 1x1 instance only, whole 256-column slices, no cluster (conv_default_cfg)
+        if not (v.mode == "tf32" and v.cg == 2 and v.cluster == 1 and layer.R == 1 and
+                layer.S == 1 and layer.K % 256 == 0):
+            return False
+    elif (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
         return False
     if ct % v.cg:
         return False
@@ -140,7 +147,7 @@ def engine_geometry(layer, v: TileVariant, n_images: int, sms: int = 148) -> dic
     num_kb = layer.R if _is_stem(layer) else ((layer.C_alloc // 16) // v.cg) * layer.R * layer.S
     g.update(flat=flat, bw=bw, bh=bh, bni=bni, rows_valid=rows, m_eff=rows / 128.0,
              m_tiles=m_tiles, n_tiles=n_tiles, tiles=m_tiles * n_tiles, num_kb=num_kb,
-             seg_kb=max(1, _SEG_ELEMS // g["ks"]), tiles_concurrent=sms,
+             seg_kb=num_kb if v.bn > 128 else max(1, _SEG_ELEMS // g["ks"]), tiles_concurrent=sms,
              tile_rows_in=(bh - 1) * layer.stride + layer.R)
     return g
 

@@ -1,0 +1,15 @@
+set -x
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"
+tail -3 gpurun_out/pytest_gpu.log
+for i in 1 2; do
+PDL_LIB=$PWD/build/libpdl_head.so python bench.py --mode tf32 > gpurun_out/ab_head_$i.json 2>gpurun_out/ab_head_$i.err
+python bench.py --mode tf32 > gpurun_out/ab_new_$i.json 2>gpurun_out/ab_new_$i.err
+done
+python - <<'P'
+import json
+for t in ("head","new"):
+    for i in (1,2):
+        d=json.loads(open(f"gpurun_out/ab_{t}_{i}.json").read().strip().splitlines()[-1])
+        pl={x["layer"]:x["ms"] for x in d.get("per_layer",[])}
+        print(t,i,d["value"],d["ms_per_step"], " ".join(f"{k.split('_')[0]}:{v}" for k,v in pl.items()))
+P
