@@ -452,10 +452,12 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
     // (1x1 layers with <= 128 input channels keep 32-channel blocks: with only 1-2
     // k-blocks per tile they lose the k-loop pipelining -- layers 2/4/8 were 3-4% slower)
     if ((flags & PDL_MODE_MASK) == PDL_MODE_TF32 && CT % 4 == 0 && (R * S > 1 || CT >= 16)) cg = 4;
-    // TF32 1x1 convs with K >= 256: 256-column tiles (one N=256 MMA per K step, half the A
-    // fill per flop; streaming epilogue), 32-channel k-blocks (48 KB stages)
+    // TF32 convs with K % 256 == 0: 256-column tiles (one N=256 MMA per K step, half the A
+    // fill per flop; streaming epilogue), 32-channel k-blocks (48 KB stages), no halo mode
+    // (its TS MMAs need TMEM columns the two 256-column accumulators use).  1x1 layers
+    // 10-21% faster in the suite; 3x3 layers 12/17 151 -> 135 / 168 -> 132 us isolated.
     // (not when the caller asks for a multicast cluster or split-K, which 256 tiles lack)
-    if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_TF32 && R == 1 && S == 1 && K % 256 == 0 && CT % 2 == 0) {
+    if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_TF32 && K % 256 == 0 && CT % 2 == 0) {
         c->bn = 256;
         cg = 2;
     }
@@ -665,7 +667,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // (3xTF32: not with 64-channel k-blocks -- two 64 KB halo buffers leave 2 weight stages,
     // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
     // TF32 stages carry one weight plane, so 64-channel k-blocks keep 4 stages.)
-    const bool halo = !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 &&
+    const bool halo = !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 && cfg.bn <= 128 &&
                       (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;

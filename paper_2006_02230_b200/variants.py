@@ -5,8 +5,8 @@ On the CPU a variant is a tiled / interchanged loop nest emitted as C.  On the
 B200 the loop nest is fixed (the persistent tile engine), and what varies is
 the tile configuration a `pdl_tile_cfg` carries:
 
-  bn       output channels (conv K / GEMM N) per CTA tile: 64 | 128 | 256 (TF32 1x1
-           convs only: one accumulation segment per tile, streaming epilogue)
+  bn       output channels (conv K / GEMM N) per CTA tile: 64 | 128 | 256 (TF32 only:
+           one accumulation segment per tile, streaming epilogue)
   bk       reduction elements per pipeline stage: 16 * cg, cg in {1, 2, 4}
   cluster  CTAs sharing (multicasting) each weight tile: 1 | 2 | 4
   mode     "3xtf32" | "tf32"
@@ -73,9 +73,8 @@ def legal(layer, v: TileVariant) -> bool:
         return v.bn == 64 and v.cluster == 1 and v.bk == 32
     ct = (layer.C + 15) // 16
     if v.bn == 256:
-        # TF32 1x1 instance only, whole 256-column slices, no cluster (conv_default_cfg)
-        if not (v.mode == "tf32" and v.cg == 2 and v.cluster == 1 and layer.R == 1 and
-                layer.S == 1 and layer.K % 256 == 0):
+        # TF32 instance only, whole 256-column slices, no cluster (conv_default_cfg)
+        if not (v.mode == "tf32" and v.cg == 2 and v.cluster == 1 and layer.K % 256 == 0):
             return False
     elif (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
         return False

@@ -1,4 +1,4 @@
-set -x
+# same-box A/B of the TF32 suite: build/libpdl_head.so (previous default) vs the tree's libpdl.so
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"
 tail -3 gpurun_out/pytest_gpu.log
 for i in 1 2; do
@@ -10,6 +10,5 @@ import json
 for t in ("head","new"):
     for i in (1,2):
         d=json.loads(open(f"gpurun_out/ab_{t}_{i}.json").read().strip().splitlines()[-1])
-        pl={x["layer"]:x["ms"] for x in d.get("per_layer",[])}
-        print(t,i,d["value"],d["ms_per_step"], " ".join(f"{k.split('_')[0]}:{v}" for k,v in pl.items()))
+        print(t, i, d["value"], d["ms_per_step"])
 P

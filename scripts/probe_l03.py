@@ -20,6 +20,8 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
     menu = [("default", None), ("no_halo", {"raster": 16})]
     if mode == "tf32" and l.K >= 128:
         menu += [("bk64", {"bk": 64}), ("bk32", {"bk": 32})]
+    if mode == "tf32" and l.K % 256 == 0:
+        menu += [("bn256_no_halo", {"bn": 256, "bk": 32, "raster": 16}), ("bk32_no_halo", {"bk": 32, "raster": 16})]
     elif mode == "3xtf32" and l.K >= 128:
         menu += [("bk64", {"bk": 64})]
     if "--pairs" in sys.argv:
@@ -35,6 +37,11 @@ for idx in [int(a) for a in sys.argv[1:] if a.isdigit()] or [3]:
             print(name, "error", e)
             continue
         torch.cuda.synchronize()
+        if cfg is None:
+            y_ref = y.clone()
+        else:
+            err = float((y - y_ref).abs().max() / y_ref.abs().max())
+            print(f"  {name}: rel diff vs default {err:.2e}")
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):

@@ -249,23 +249,26 @@ def test_bad_shapes_raise(P):
         P.conv2d_nchw16c(torch.zeros((1, 2, 4, 4, 16), device="cuda"), w)
 
 
-@pytest.mark.parametrize("shape", [(3, 64, 256, 7, 1), (2, 96, 512, 9, 1), (1, 256, 768, 14, 2),
-                                   (5, 512, 256, 5, 1), (2, 32, 1024, 28, 2)])
+@pytest.mark.parametrize("shape", [(3, 64, 256, 7, 1, 1), (2, 96, 512, 9, 1, 1), (1, 256, 768, 14, 2, 1),
+                                   (5, 512, 256, 5, 1, 1), (2, 32, 1024, 28, 2, 1), (2, 16, 256, 9, 1, 3),
+                                   (3, 64, 512, 7, 1, 3), (2, 32, 256, 15, 2, 3), (1, 32, 256, 12, 1, 5)])
 def test_tf32_wide_tiles(P, shape):
-    """TF32 1x1 convs with K % 256 == 0 default to 256-column tiles (streaming epilogue);
-    ragged pixel tails, strides and channel counts against the oracle and the 128-column
-    tiles (bitwise while C <= 256 keeps both in one accumulation segment)."""
-    n, C, K, H, stride = shape
+    """TF32 convs with K % 256 == 0 default to 256-column tiles (streaming epilogue);
+    ragged pixel tails, strides, filter sizes and channel counts against the oracle and
+    the 128-column tiles (bitwise while C*R*S <= 256 keeps both in one accumulation
+    segment)."""
+    n, C, K, H, stride, R = shape
+    pad = R // 2
     rng = np.random.default_rng(sum(shape))
     x = (rng.random((n, C // 16, H, H, 16), np.float32) * 2 - 1).astype(np.float32)
-    w = ((rng.random((K // 16, C // 16, 1, 1, 16, 16)) * 2 - 1) / np.sqrt(C)).astype(np.float32)
+    w = ((rng.random((K // 16, C // 16, R, R, 16, 16)) * 2 - 1) / np.sqrt(C * R * R)).astype(np.float32)
     b = rng.random(K, np.float32)
-    ref = oracle.conv2d_f64(x, w, b, stride=stride, pad=0, relu=True)
-    kw = dict(stride=stride, pad=0, relu=True, mode="tf32")
+    ref = oracle.conv2d_f64(x, w, b, stride=stride, pad=pad, relu=True)
+    kw = dict(stride=stride, pad=pad, relu=True, mode="tf32")
     wide = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), **kw)
     assert rel(wide.cpu().numpy(), ref) <= TOL["tf32"]
-    narrow = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), cfg={"bn": 128, "bk": 32, "split_k": 1}, **kw)
-    if C <= 256:
+    narrow = P.conv2d_nchw16c(cuda(x), cuda(w), cuda(b), cfg={"bn": 128, "bk": 32 if C % 32 == 0 else 16, "split_k": 1}, **kw)
+    if C * R * R <= 256:
         assert torch.equal(wide, narrow)
     else:
         assert rel(wide.cpu().numpy(), narrow.cpu().numpy().astype(np.float64)) <= 1e-5
