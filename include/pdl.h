@@ -75,6 +75,12 @@ typedef struct pdl_tile_cfg {
 enum {
     PDL_BIAS = 1,             /* y += bias[k]                                  */
     PDL_RELU = 2,             /* y = max(y, 0)   (after bias)                  */
+    PDL_RELU6 = 1 << 2,       /* y = min(max(y, 0), 6)   (after bias; ReLU6 of
+                                 PAPER.md:1233-1234)                           */
+    PDL_SCALE = 1 << 3,       /* y *= scale[k] before the bias (batch-norm
+                                 inference affine): `bias`
+                                 then holds 2*K floats, shift[K] then scale[K];
+                                 the shift is added only with PDL_BIAS         */
     PDL_MODE_3XTF32 = 0 << 4, /* default                                       */
     PDL_MODE_TF32 = 1 << 4,
     PDL_MODE_FP32 = 2 << 4,

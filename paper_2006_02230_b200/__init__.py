@@ -16,5 +16,7 @@ from .loopnest import (LoopDslError, LoopNest, NonAffineError, ParseError, Progr
                        parse, parse_program, pretty, reinstate_microkernel,
                        substitute_microkernel)
 from .executor import InterpreterError, execute, interpret, make_inputs, plan_program  # noqa: F401
+from .fusion import (FusedNest, FusionDecision, FusionError, OperatorPair, can_fuse,  # noqa: F401
+                     fuse, write_set)
 
 __version__ = "0.1.0"

@@ -15,6 +15,8 @@ LIB_PATH = os.environ.get("PDL_LIB") or os.path.join(_PKG, "libpdl.so")
 
 PDL_BIAS = 1
 PDL_RELU = 2
+PDL_RELU6 = 1 << 2
+PDL_SCALE = 1 << 3
 PDL_MODE_3XTF32 = 0 << 4
 PDL_MODE_TF32 = 1 << 4
 PDL_MODE_FP32 = 2 << 4

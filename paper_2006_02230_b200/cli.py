@@ -150,17 +150,40 @@ def cmd_emit(a) -> int:
 
 
 def cmd_fuse(a) -> int:
+    """Alg. 3 on the first two operators of the program (heavy, element-wise, in
+    either order; nests between them are the intervening code): the decision with
+    its witness, the fused `.pdl` when fusable (--emit-pdl FILE or DIR/fused.pdl),
+    and the executor's kernel plan (which epilogue the fused kernel applies)."""
+    from . import fusion as F
     from .executor import ConvPlan, EltwisePlan, GemmPlan, plan_program
-    plans = plan_program(_load(a.file), a.binding)
+    nests = _load(a.file)
+    if len(nests) < 2:
+        raise _Usage("fuse needs a program of two operators")
+    first_ew = not nests[0].has_kernel_call() and any(
+        s.op == "=" for s in nests[0].statements()) and any(s.op == "+=" for s in nests[-1].statements())
+    pair = F.OperatorPair(nests[-1], nests[0], tuple(nests[1:-1]), ew_first=True) if first_ew \
+        else F.OperatorPair(nests[0], nests[-1], tuple(nests[1:-1]))
+    d = F.can_fuse(pair, a.binding, strict=a.strict)
+    fused_text = L.pretty(F.fuse(pair, a.binding, strict=a.strict)) if d.fusable else None
+    if fused_text is not None:
+        dst = a.emit_pdl or (a.out and os.path.join(a.out, "fused.pdl"))
+        if dst:
+            with open(dst, "w") as fh:
+                fh.write(fused_text)
+    plans = plan_program(nests, a.binding) if len(nests) == 2 else []
     rows = []
     for p in plans:
         kind = "conv" if isinstance(p, ConvPlan) else "gemm" if isinstance(p, GemmPlan) else "eltwise"
         ep = getattr(p, "epilogue", None)
         rows.append({"nest": p.nest, "kind": kind,
                      "fused_epilogue": None if ep is None else {
-                         "nest": ep.nest, "bias": ep.bias is not None, "relu": ep.relu,
-                         "relu6": ep.relu6}})
-    print(_dump({"version": REPORT_VERSION, "file": os.path.basename(a.file), "plans": rows},
+                         "nest": ep.nest, "bias": ep.bias is not None, "scale": ep.scale is not None,
+                         "relu": ep.relu, "relu6": ep.relu6}})
+    wit = d.witness
+    print(_dump({"version": REPORT_VERSION, "file": os.path.basename(a.file),
+                 "decision": {"fusable": d.fusable, "failed": d.failed, "detail": d.detail,
+                              "witness": None if wit is None else json.loads(json.dumps(wit, default=list))},
+                 "fused_pdl": fused_text, "plans": rows},
                 a.out and os.path.join(a.out, "fusion.json")), end="")
     return 0
 
@@ -214,8 +237,11 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--variant", required=True)
     p.add_argument("--mode", default="3xtf32", choices=["3xtf32", "tf32"])
     p.set_defaults(fn=cmd_emit)
-    p = sub.add_parser("fuse", help="Alg. 3 fusion plan of a program")
+    p = sub.add_parser("fuse", help="Alg. 3: can_fuse decision, fused .pdl, kernel plan")
     common(p)
+    p.add_argument("--emit-pdl", default=None, help="write the fused nest here")
+    p.add_argument("--strict", action="store_true",
+                   help="also refuse intervening writes to the element-wise operator's inputs")
     p.set_defaults(fn=cmd_fuse)
     p = sub.add_parser("train", help="train the pairwise judge from a dataset CSV")
     p.add_argument("file")

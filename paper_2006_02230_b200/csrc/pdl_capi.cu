@@ -111,10 +111,11 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // Persistent launch: grid = as many CTAs (clusters of CL) as can be co-resident,
 // capped by the work.  Clusters of 4 cannot use every SM (GPC granularity), so
 // the co-resident count comes from cudaOccupancyMaxActiveClusters.
-template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0, bool HALO = false>
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0, bool HALO = false,
+          bool EPIX = false>
 int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_ctas, cudaStream_t s) {
     using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
-    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR, RESW, HALO>;
+    auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR, RESW, HALO, EPIX>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_ctas = 0;
@@ -185,6 +186,29 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         }
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
+}
+
+// Extended-epilogue instances (PDL_SCALE / PDL_RELU6): cluster 1, no pairs, resident
+// weights, halo or 256-column tiles (the host picks a plain schedule for these calls)
+template <int KIND, bool SPLIT3>
+int dispatch_epix(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams &p, cudaStream_t s) {
+    const int work = p.m_tiles * p.n_tiles * std::max(1, p.split);
+    if constexpr (KIND == pdl::KIND_STEM) {
+        if (bn == 64 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 64 && cg == pdl::kStemPackedCG)
+            return launch_tile<KIND, 64, pdl::kStemPackedCG, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+    } else if constexpr (KIND == pdl::KIND_GEMM) {
+        if (bn == 64) return launch_tile<KIND, 64, 1, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 128) return launch_tile<KIND, 128, 1, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+    } else {
+        if (bn == 64 && cg == 1) return launch_tile<KIND, 64, 1, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 64 && cg == 2) return launch_tile<KIND, 64, 2, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 64 && cg == 4) return launch_tile<KIND, 64, 4, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 128 && cg == 1) return launch_tile<KIND, 128, 1, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 128 && cg == 2) return launch_tile<KIND, 128, 2, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+        if (bn == 128 && cg == 4) return launch_tile<KIND, 128, 4, SPLIT3, 1, false, 0, false, true>(maps, p, work, s);
+    }
+    return fail(PDL_EUNSUPPORTED, "no extended-epilogue instance for bn=%d cg=%d", bn, cg);
 }
 
 // Resident-weight 1x1 conv instances (3xTF32, cluster 1): RESW bytes per plane
@@ -335,6 +359,7 @@ size_t gemm_split_bytes(int M, int N, int K, unsigned flags, const pdl_tile_cfg 
     if (M <= 0 || N <= 0 || K <= 0 || (flags & PDL_MODE_MASK) == PDL_MODE_FP32) return 0;
     int bn, cl, raster;
     gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
+    if (flags & PDL_RELU6) cl = 1;  // extended-epilogue instances are cluster 1
     if (cl != 1 && cl != 2 && cl != 4) return 0;
     return plan_split((M + 127) / 128, (N + bn - 1) / bn, cl, bn, (K + 31) / 32, kSegElems / 32,
                       cfg_in ? cfg_in->split_k : 0).bytes;
@@ -588,6 +613,9 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     p.n_tiles = (K + bn - 1) / bn;
     // the grid is a multiple of n_tiles: every CTA keeps one N-tile (resident weights)
     const int scg = stem_packed(C, R, S) ? pdl::kStemPackedCG : 1;
+    if (flags & (PDL_SCALE | PDL_RELU6))
+        return split ? dispatch_epix<pdl::KIND_STEM, true>(bn, scg, maps, p, st)
+                     : dispatch_epix<pdl::KIND_STEM, false>(bn, scg, maps, p, st);
     if (split) return dispatch_tile<pdl::KIND_STEM, true>(bn, scg, 1, maps, p, st);
     return dispatch_tile<pdl::KIND_STEM, false>(bn, scg, 1, maps, p, st);
 }
@@ -618,6 +646,13 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         if (cfg_in->cluster_n) cfg.cluster_n = cfg_in->cluster_n;
         cfg.raster = cfg_in->raster;
     }
+    // scale / ReLU6 epilogue: the plain schedule of the EPIX instances (cluster 1, at most
+    // 128 columns; no pairs, resident weights or halo)
+    const bool epix = flags & (PDL_SCALE | PDL_RELU6);
+    if (epix) {
+        if (cfg.bn > 128) cfg.bn = 128;
+        cfg.cluster_m = cfg.cluster_n = 1;
+    }
     // cluster_n == 2: the tile is computed by a CTA pair with cta_group::2 MMAs
     // (M = 256, each CTA holds half of B); 3xTF32 only
     const bool pair = cfg.cluster_n == 2 && split;
@@ -625,7 +660,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // 1x1 convs whose N-tile weight slice fits in 64 KB per plane keep it resident
     // (loaded once per CTA; stages carry A only) unless a multicast cluster is asked for
     const int res_plane = ceil16(C) * 16 * cfg.bn * 4;
-    const bool resident = split && !pair && R == 1 && S == 1 && cfg.bk == 32 && res_plane <= 65536 &&
+    const bool resident = split && !pair && !epix && R == 1 && S == 1 && cfg.bk == 32 && res_plane <= 65536 &&
                           (!cfg_in || cfg_in->cluster_m <= 1);
     if (resident) cfg.cluster_m = 1;
     const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16;
@@ -641,7 +676,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // segment tiles: no weight multicast by default (pairs of CTAs in lockstep wait for
     // the one whose tile spans two images; cluster 1 measured 4-9% faster on ResNet
     // layers 12/13/15 at 256 images)
-    if (g.seg_mode && !(cfg_in && cfg_in->cluster_m)) cl = 1;
+    if ((g.seg_mode && !(cfg_in && cfg_in->cluster_m)) || epix) cl = 1;
     const int m_tiles = g.m_tiles, n_tiles = (K + cfg.bn - 1) / cfg.bn;
     const int num_kb = (CT / cg) * R * S;
     // BN=256 (TF32): one accumulation segment per tile, never split (streaming epilogue)
@@ -667,7 +702,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // (3xTF32: not with 64-channel k-blocks -- two 64 KB halo buffers leave 2 weight stages,
     // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
     // TF32 stages carry one weight plane, so 64-channel k-blocks keep 4 stages.)
-    const bool halo = !pair && !resident && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 && cfg.bn <= 128 &&
+    const bool halo = !pair && !resident && !epix && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 &&
+                      cfg.bn <= 128 &&
                       (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
@@ -776,6 +812,9 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         p.res_bytes = res_plane;
         return dispatch_resident(cfg.bn, cg, res_plane, maps, p, st);
     }
+    if (epix)
+        return split ? dispatch_epix<pdl::KIND_CONV, true>(cfg.bn, cg, maps, p, st)
+                     : dispatch_epix<pdl::KIND_CONV, false>(cfg.bn, cg, maps, p, st);
     if (split) return dispatch_tile<pdl::KIND_CONV, true>(cfg.bn, cg, cl, maps, p, st);
     return dispatch_tile<pdl::KIND_CONV, false>(cfg.bn, cg, cl, maps, p, st);
 }
@@ -877,8 +916,8 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
     int rc;
     if ((rc = device_check())) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
-    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
-        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
         return fail(PDL_EUNSUPPORTED, "conv: PDL_MODE_FP32 takes raw weights (pdl_conv2d_fwd_nchw16c)");
     if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
@@ -905,8 +944,8 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
     int rc;
     if ((rc = device_check())) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
-    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
-        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
         return fail(PDL_EUNSUPPORTED, "conv: PDL_MODE_FP32 takes raw weights (pdl_conv2d_fwd_nchw16c)");
     if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
@@ -937,8 +976,8 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     if (chunk < 0) return fail(PDL_EINVAL, "conv host: negative chunk");
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
         return fail(PDL_EUNSUPPORTED, "conv host: PDL_MODE_FP32 takes raw weights (pdl_conv2d_fwd_nchw16c)");
-    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
-        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
     if (!aligned16(packed_w) || !aligned16(workspace))
         return fail(PDL_EALIGN, "conv host: packed weights / workspace unaligned");
     // shape checks before anything is enqueued (workspace stands in for x / y)
@@ -1017,8 +1056,8 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
     int rc;
     if ((rc = device_check())) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
-    if ((flags & PDL_BIAS) && (!bias || !aligned16(bias)))
-        return fail(PDL_EALIGN, "conv: PDL_BIAS needs a 16-byte aligned bias");
+    if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
     cudaStream_t st = (cudaStream_t)stream;
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32) {
         const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
@@ -1067,6 +1106,8 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     if ((rc = get_encode())) return rc;
     int bn, cl, raster;
     gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
+    const bool epix = flags & PDL_RELU6;  // extended-epilogue instances are cluster 1
+    if (epix) cl = 1;
     if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "gemm: cluster_m must be 1, 2 or 4");
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -1102,6 +1143,9 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
                                          workspace ? req : (req > 1 ? req : 1));
         if ((rc = bind_split(p, spl, workspace, ws_bytes, cl))) return rc;
     }
+    if (epix)
+        return mode == PDL_MODE_3XTF32 ? dispatch_epix<pdl::KIND_GEMM, true>(bn, 1, maps, p, st)
+                                       : dispatch_epix<pdl::KIND_GEMM, false>(bn, 1, maps, p, st);
     if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, cl, maps, p, st);
     return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, cl, maps, p, st);
 }
@@ -1112,13 +1156,13 @@ int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int 
     int rc;
     if ((rc = device_check())) return rc;
     if (K % 16 || N < 0 || P < 0 || Q < 0) return fail(PDL_EINVAL, "bias_relu: bad shape");
-    if (!aligned16(y) || ((flags & PDL_BIAS) && (!bias || !aligned16(bias))))
+    if (!aligned16(y) || ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias))))
         return fail(PDL_EALIGN, "bias_relu: unaligned pointer");
     const long long n4 = (long long)N * K * P * Q / 4;
     if (n4 == 0) return PDL_OK;
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, 148LL * 8);
     pdl::bias_relu_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-        reinterpret_cast<float4 *>(y), reinterpret_cast<const float4 *>(bias), n4, P * Q, K / 16, flags);
+        reinterpret_cast<float4 *>(y), bias, n4, P * Q, K / 16, flags);
     ++g_launches;
     return check_launch("bias_relu_kernel");
 }

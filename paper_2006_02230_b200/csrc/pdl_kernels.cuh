@@ -290,12 +290,63 @@ __device__ __forceinline__ void split_lo_smem(uint32_t src, uint32_t lo, int byt
     }
 }
 
+// Fused element-wise epilogue of Alg. 3 on output column(s) from
+// `col`, in the reference's order of operations: PDL_SCALE multiplies by scale[k]
+// (batch-norm inference affine, scale stored after the K shifts in `bias`), PDL_BIAS
+// adds bias[k], PDL_RELU is Python's max(v, 0.0) (keep v unless 0 > v), PDL_RELU6 is
+// min(max(v, 0.0), 6.0) (keep v unless 6 < v).  Columns >= n_out read nothing.
+__device__ __forceinline__ float epi_relu(unsigned f, float v) {
+    if (f & (PDL_RELU | PDL_RELU6)) v = (0.f > v) ? 0.f : v;
+    if (f & PDL_RELU6) v = (6.f < v) ? 6.f : v;
+    return v;
+}
+__device__ __forceinline__ float epilogue1(unsigned f, const float *bias, int n_out, int col, float v) {
+    if (bias && col < n_out) {
+        if (f & PDL_SCALE) v = __fmul_rn(v, __ldg(bias + n_out + col));
+        if (f & PDL_BIAS) v = __fadd_rn(v, __ldg(bias + col));
+    }
+    return epi_relu(f, v);
+}
+// FULL = false: bias + ReLU only.  The tile kernels compile it into their default
+// instances and get the scale / ReLU6 form only in separate EPIX instances: even
+// one extra select per element in the epilogue loop moved the output-heavy layers
+// (stem, 2, 4, 8) by 4-16% (register allocation / code layout of the big kernel),
+// measured with scripts/ab_libs.sh.
+template <bool FULL>
+__device__ __forceinline__ float4 epilogue4(unsigned f, const float *bias, int n_out, int col, float4 r) {
+    if constexpr (FULL) {
+        if (bias && col < n_out) {
+            if (f & PDL_SCALE) {
+                const float4 s = __ldg(reinterpret_cast<const float4 *>(bias + n_out + col));
+                r.x = __fmul_rn(r.x, s.x); r.y = __fmul_rn(r.y, s.y);
+                r.z = __fmul_rn(r.z, s.z); r.w = __fmul_rn(r.w, s.w);
+            }
+            if (f & PDL_BIAS) {
+                const float4 b = __ldg(reinterpret_cast<const float4 *>(bias + col));
+                r.x = __fadd_rn(r.x, b.x); r.y = __fadd_rn(r.y, b.y);
+                r.z = __fadd_rn(r.z, b.z); r.w = __fadd_rn(r.w, b.w);
+            }
+        }
+        r.x = epi_relu(f, r.x); r.y = epi_relu(f, r.y); r.z = epi_relu(f, r.z); r.w = epi_relu(f, r.w);
+    } else {
+        if ((f & PDL_BIAS) && bias && col < n_out) {
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(bias + col));
+            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+        }
+        if (f & PDL_RELU) {
+            r.x = (0.f > r.x) ? 0.f : r.x;
+            r.y = (0.f > r.y) ? 0.f : r.y;
+            r.z = (0.f > r.z) ? 0.f : r.z;
+            r.w = (0.f > r.w) ? 0.f : r.w;
+        }
+    }
+    return r;
+}
+
 // Epilogue for 16 consecutive output columns [col0, col0+16) of one row.
-template <int KIND>
+template <int KIND, bool EPIX>
 __device__ __forceinline__ void store16(const TileParams &p, float *dst, int col0,
                                         const float *v) {
-    const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
-    const bool relu = p.flags & PDL_RELU;
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
         const int col = col0 + q4 * 4;
@@ -309,16 +360,7 @@ __device__ __forceinline__ void store16(const TileParams &p, float *dst, int col
                 r.z += p.beta * c.z; r.w += p.beta * c.w;
             }
         }
-        if (has_bias) {
-            const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col));
-            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
-        }
-        if (relu) {  // Python max(v, 0.0): keep v unless 0 > v
-            r.x = (0.f > r.x) ? 0.f : r.x;
-            r.y = (0.f > r.y) ? 0.f : r.y;
-            r.z = (0.f > r.z) ? 0.f : r.z;
-            r.w = (0.f > r.w) ? 0.f : r.w;
-        }
+        r = epilogue4<EPIX>(p.flags, p.bias, p.n_out, col, r);
         *reinterpret_cast<float4 *>(dst + q4 * 4) = r;
     }
 }
@@ -419,7 +461,9 @@ __device__ __forceinline__ void stem_gather_kb(int c, uint32_t sa, uint32_t row_
     }
 }
 
-template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0, bool HALO = false>
+// EPIX: the extended fused epilogue (PDL_SCALE, PDL_RELU6) -- separate instances, see epilogue4
+template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int RESW = 0, bool HALO = false,
+          bool EPIX = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tile_mma_kernel(const __grid_constant__ TmaMaps maps, const TileParams p) {
     static_assert(CL == 1 || KIND != KIND_STEM, "the stem keeps its weights resident");
@@ -1047,8 +1091,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t ebase = smem0 + L::EPI_OFF + half * L::EPI_BUFS * 8192;
                 const bool in_box = row < p.BW * p.BH * p.BNI;
                 const bool leader = quarter == 0 && lane == 0;
-                const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
-                const bool relu = p.flags & PDL_RELU;
 #pragma unroll 1
                 for (int j = 0; j < HALF / 16; ++j) {
                     float v[16];
@@ -1067,16 +1109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4) {
                             float4 r = make_float4(v[q4 * 4], v[q4 * 4 + 1], v[q4 * 4 + 2], v[q4 * 4 + 3]);
-                            if (has_bias && col0 < p.n_out) {
-                                const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col0 + q4 * 4));
-                                r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
-                            }
-                            if (relu) {
-                                r.x = (0.f > r.x) ? 0.f : r.x;
-                                r.y = (0.f > r.y) ? 0.f : r.y;
-                                r.z = (0.f > r.z) ? 0.f : r.z;
-                                r.w = (0.f > r.w) ? 0.f : r.w;
-                            }
+                            r = epilogue4<EPIX>(p.flags, p.bias, p.n_out, col0 + q4 * 4, r);
                             sts128(ebuf + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4), r);
                         }
                     }
@@ -1199,8 +1232,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // free), then lane t stores 16 bytes of pixel 8i + t/4: 512 contiguous bytes
                 // per instruction wherever the pixels are consecutive in y
                 const uint32_t wbuf = smem0 + L::EPI_OFF + (uint32_t)e * 2048;
-                const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
-                const bool relu = p.flags & PDL_RELU;
                 const int per_img = p.BW * p.BH;
                 const size_t plane = (size_t)p.P * p.Q * 16;
                 // output pixel offsets (floats, channel block 0) of the 4 pixels this lane stores
@@ -1222,16 +1253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int q4 = 0; q4 < 4; ++q4) {
                         float4 r = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
                                                sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
-                        if (has_bias) {
-                            const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col0 + q4 * 4));
-                            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
-                        }
-                        if (relu) {
-                            r.x = (0.f > r.x) ? 0.f : r.x;
-                            r.y = (0.f > r.y) ? 0.f : r.y;
-                            r.z = (0.f > r.z) ? 0.f : r.z;
-                            r.w = (0.f > r.w) ? 0.f : r.w;
-                        }
+                        r = epilogue4<EPIX>(p.flags, p.bias, p.n_out, col0 + q4 * 4, r);
                         sts128(wbuf + lane * 64 + ((q4 ^ ((lane >> 1) & 3)) << 4), r);
                     }
                     __syncwarp();
@@ -1255,8 +1277,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t ebase = smem0 + L::EPI_OFF + half * L::EPI_BUFS * 8192;
                 const bool in_box = row < p.BW * p.BH * p.BNI;
                 const bool leader = quarter == 0 && lane == 0;
-                const bool has_bias = (p.flags & PDL_BIAS) && p.bias;
-                const bool relu = p.flags & PDL_RELU;
                 // one 16-channel output box of this tile from smem buffer `ebuf`
                 auto store_box = [&](uint32_t ebuf, int col0) {
                     if (col0 >= p.n_out || (p.flags & DBG_NO_EPI_STORE)) {
@@ -1281,16 +1301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int q4 = 0; q4 < 4; ++q4) {
                         float4 r = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
                                                sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
-                        if (has_bias && col0 < p.n_out) {
-                            const float4 b = __ldg(reinterpret_cast<const float4 *>(p.bias + col0 + q4 * 4));
-                            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
-                        }
-                        if (relu) {
-                            r.x = (0.f > r.x) ? 0.f : r.x;
-                            r.y = (0.f > r.y) ? 0.f : r.y;
-                            r.z = (0.f > r.z) ? 0.f : r.z;
-                            r.w = (0.f > r.w) ? 0.f : r.w;
-                        }
+                        r = epilogue4<EPIX>(p.flags, p.bias, p.n_out, col0 + q4 * 4, r);
                         sts128(ebuf + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4), r);
                     }
                 };
@@ -1359,7 +1370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (col0 < p.n_out) {
                         float *dst = KIND == KIND_GEMM ? obase + col0
                                                        : obase + (size_t)(col0 >> 4) * cstride;
-                        store16<KIND>(p, dst, col0, &sum[j * 16]);
+                        store16<KIND, EPIX>(p, dst, col0, &sum[j * 16]);
                     }
                 }
             }
@@ -1428,9 +1439,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const float *__restrict_
             if (gn >= N) continue;
             float r = alpha * acc[i][j];
             if (beta != 0.f) r += beta * C[(size_t)gm * ldc + gn];
-            if ((flags & PDL_BIAS) && bias) r += bias[gn];
-            if ((flags & PDL_RELU) && 0.f > r) r = 0.f;
-            C[(size_t)gm * ldc + gn] = r;
+            C[(size_t)gm * ldc + gn] = epilogue1(flags, bias, N, gn, r);
         }
     }
 }
@@ -1472,30 +1481,18 @@ __global__ void __launch_bounds__(128) simt_conv_kernel(const float *__restrict_
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         float r = acc[k];
-        if ((flags & PDL_BIAS) && bias) r += bias[kt * 16 + k];
-        if ((flags & PDL_RELU) && 0.f > r) r = 0.f;
-        yo[k] = r;
+        yo[k] = epilogue1(flags, bias, KT * 16, kt * 16 + k, r);
     }
 }
 
-// Unfused element-wise pass y = max(y + b, 0) over nKhw16k (float4 vectorised).
-__global__ void bias_relu_kernel(float4 *__restrict__ y, const float4 *__restrict__ bias,
+// Unfused element-wise pass over nKhw16k (float4 vectorised): the same epilogue as the
+// fused kernels (scale, bias, ReLU / ReLU6).
+__global__ void bias_relu_kernel(float4 *__restrict__ y, const float *__restrict__ bias,
                                  long long n4, int pq, int KT, unsigned flags) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
          i += (long long)gridDim.x * blockDim.x) {
-        float4 v = y[i];
-        if ((flags & PDL_BIAS) && bias) {
-            const int kt = (int)((i / (4LL * pq)) % KT);
-            const float4 b = __ldg(bias + kt * 4 + (int)(i & 3));
-            v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
-        }
-        if (flags & PDL_RELU) {
-            v.x = (0.f > v.x) ? 0.f : v.x;
-            v.y = (0.f > v.y) ? 0.f : v.y;
-            v.z = (0.f > v.z) ? 0.f : v.z;
-            v.w = (0.f > v.w) ? 0.f : v.w;
-        }
-        y[i] = v;
+        const int kt = (int)((i / (4LL * pq)) % KT);
+        y[i] = epilogue4<true>(flags, bias, KT * 16, kt * 16 + (int)(i & 3) * 4, y[i]);
     }
 }
 

@@ -11,11 +11,15 @@ launches the B200 kernels:
 * the Fig. 9 blocked convolution -- any loop order, tiling
   or parallel marking of it, with or without the `#pragma microkernel` band;
 * the Fig. 1 / Fig. 12 GEMM (PAPER.md:232-243, 1112-1117);
-* an element-wise epilogue nest over the conv / GEMM output
-  (`y = max(y + b, 0.0)`, `y = max(y, 0.0)`, `y = y + b`,
-  `y = min(max(y + b, 0.0), 6.0)`), which is fused into the preceding heavy
-  nest when Alg. 3's conditions hold:
-  same write set, element-wise, nothing in between.
+* an element-wise epilogue nest over the conv / GEMM output: an optional
+  per-channel scale (batch-norm inference affine `y * s[k]`), an optional bias /
+  shift `+ b[k]`, then optionally ReLU `max(., 0.0)` or ReLU6
+  `min(max(., 0.0), 6.0)`.  It is fused into the preceding
+  heavy nest when Alg. 3's conditions hold:
+  same write set, element-wise, nothing in between -- the kernels then apply it
+  in their epilogue (PDL_SCALE / PDL_BIAS / PDL_RELU / PDL_RELU6);
+* a `fusion.FusedNest` (the output of `fusion.fuse`), executed as its operator
+  pair with the element-wise part in the kernel epilogue.
 
 Recognition is semantic, not textual: every array subscript is an affine form
 over the loop iterators; the executor assigns the iterators to the roles of the
@@ -98,6 +102,13 @@ class EltwisePlan:
     relu: bool
     relu6: bool
     bias_axes: tuple = ()   # target dims the bias is indexed by
+    scale: str | None = None
+    scale_axes: tuple = ()  # target dims the scale is indexed by
+
+    def channel_axes_ok(self, axes: tuple) -> bool:
+        """bias / scale indexed exactly by the output-channel dims `axes`."""
+        return (self.bias is None or self.bias_axes == axes) and \
+            (self.scale is None or self.scale_axes == axes)
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -268,6 +279,7 @@ def _match_gemm(nest, stmt, loops, env, shapes):
 
 
 def _match_eltwise(nest, stmt, loops, env, shapes):
+    """y = act(y * s + b) over the target, every part optional but one."""
     tgt = stmt.target
     if stmt.op != "=":
         return None
@@ -279,22 +291,34 @@ def _match_eltwise(nest, stmt, loops, env, shapes):
         relu, e = True, e.args[0]
     elif relu6:
         return None
-    bias = None
-    axes = ()
-    if isinstance(e, BinOp) and e.op == "+" and isinstance(e.left, Access) \
-            and isinstance(e.right, Access):
-        y, bacc = e.left, e.right
+
+    def axes_of(acc):
         axes = []
-        for ix in bacc.indices:
+        for ix in acc.indices:
             pos = [d for d, t in enumerate(tgt.indices) if t == ix]
             if len(pos) != 1:
                 return None
             axes.append(pos[0])
-        bias, e = bacc.array, y
-        axes = tuple(axes)
+        return tuple(axes)
+
+    bias = scale = None
+    axes = s_axes = ()
+    if isinstance(e, BinOp) and e.op == "+" and isinstance(e.right, Access):
+        axes = axes_of(e.right)
+        if axes is None:
+            return None
+        bias, e = e.right.array, e.left
+    if isinstance(e, BinOp) and e.op == "*" and isinstance(e.right, Access) \
+            and isinstance(e.left, Access) and e.left.array == tgt.array:
+        s_axes = axes_of(e.right)
+        if s_axes is None:
+            return None
+        scale, e = e.right.array, e.left
     if not (isinstance(e, Access) and e.array == tgt.array and e.indices == tgt.indices):
         return None
-    if not (relu or bias):
+    if not (relu or bias or scale):
+        return None
+    if tgt.array in (bias, scale):
         return None
     rng = _loop_ranges(loops, env)
     iters = {lp.iterator for lp in loops}
@@ -306,13 +330,42 @@ def _match_eltwise(nest, stmt, loops, env, shapes):
         return None
     if _count(list(loops), env) != int(np.prod(ext)):
         return None
-    return EltwisePlan(nest.name, tgt.array, bias, relu, relu6, axes)
+    return EltwisePlan(nest.name, tgt.array, bias, relu, relu6, axes, scale, s_axes)
+
+
+def _covers(plan, shapes) -> bool:
+    """The heavy nest writes every element of its output array."""
+    if isinstance(plan, ConvPlan):
+        return tuple(shapes[plan.out]) == (plan.N, plan.KT, plan.P, plan.Q, 16)
+    return tuple(shapes[plan.C]) == (plan.M, plan.N)
+
+
+def _expand(nests) -> list:
+    """FusedNest -> its operator pair in execution order (intervening nests after)."""
+    out = []
+    for n in nests:
+        pr = getattr(n, "pair", None)
+        if pr is None:
+            out.append(n)
+        elif pr.ew_first:
+            out += [pr.eltwise, pr.heavy, *pr.between]
+        else:
+            out += [pr.heavy, pr.eltwise, *pr.between]
+    return out
 
 
 def plan_program(nests: Sequence[LoopNest], binding: Mapping[str, int]) -> list:
-    """Recognise every nest; fuse element-wise nests into the preceding heavy one
-    when Alg. 3's conditions hold (same write set, element-wise, adjacent)."""
+    """Recognise every nest; fuse an element-wise nest into the preceding heavy one
+    when Alg. 3's conditions hold.  They are checked structurally on the matched
+    nests (fusion.can_fuse enumerates, which only suits desk-sized bindings):
+    (1) W_hy = W_ew -- the element-wise nest targets the heavy nest's output array
+        and both cover all of it (the matchers prove each nest onto its array);
+    (2) element-wise -- matched as one instance per element (count = |array|,
+        injective subscripts), reading the target only at the element it writes;
+    (3) nothing in between -- the nests are adjacent in the program."""
+    nests = _expand(nests)
     plans: list = []
+    shapes_all: dict = {}
     for nest in nests:
         if nest.has_kernel_call():
             if nest.microkernel is None:
@@ -321,6 +374,7 @@ def plan_program(nests: Sequence[LoopNest], binding: Mapping[str, int]) -> list:
         if any(isinstance(n, KernelCall) for n in walk(nest.body)):
             raise InterpreterError(f"cannot execute opaque kernel call in {nest.name!r}")
         shapes = nest.shapes(binding)
+        shapes_all.update(shapes)
         env = {p: int(binding[p]) for p in nest.params}
         stmt, loops = _single_stmt(nest)
         for acc in (stmt.target,) + stmt.read_accesses():
@@ -337,10 +391,8 @@ def plan_program(nests: Sequence[LoopNest], binding: Mapping[str, int]) -> list:
                 and plans[-1].epilogue is None:
             heavy = plans[-1]
             out = heavy.out if isinstance(heavy, ConvPlan) else heavy.C
-            ok_axes = (plan.bias is None or
-                       (isinstance(heavy, ConvPlan) and plan.bias_axes == (1, 4)) or
-                       (isinstance(heavy, GemmPlan) and plan.bias_axes == (1,)))
-            if plan.target == out and ok_axes and not plan.relu6:
+            axes = (1, 4) if isinstance(heavy, ConvPlan) else (1,)
+            if plan.target == out and plan.channel_axes_ok(axes) and _covers(heavy, shapes_all):
                 heavy.epilogue = plan
                 continue
         plans.append(plan)
@@ -362,6 +414,16 @@ def _as_float32_device(torch, arr, shape, device):
     return t.reshape(shape).to(device)
 
 
+def _epilogue_args(ep, arrays, K: int) -> dict:
+    """ops keyword arguments of an element-wise plan (device bias / scale vectors)."""
+    if ep is None:
+        return {}
+    def vec(name):
+        return None if name is None else arrays[name].reshape(-1)[:K].contiguous()
+    return {"bias": vec(ep.bias), "scale": vec(ep.scale), "relu": ep.relu and not ep.relu6,
+            "relu6": ep.relu6}
+
+
 def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
             mode: str = "3xtf32", device=None, keep_on_device: bool = False) -> dict:
     """Run a nest / Program on the GPU.  Returns {array: flat float64 ndarray}
@@ -373,6 +435,7 @@ def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
         nests = list(nests.nests)
     elif isinstance(nests, LoopNest):
         nests = [nests]
+    nests = _expand(nests)
     missing = sorted({p for n in nests for p in n.params if p not in binding})
     if missing:
         raise UnboundParameterError(f"unbound parameters: {missing}")
@@ -395,22 +458,16 @@ def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
             x = arrays[plan.inp][:plan.N]
             w = arrays[plan.filt]
             ep = plan.epilogue
-            bias = None
-            if ep is not None and ep.bias is not None:
-                bias = arrays[ep.bias].reshape(-1)[:plan.KT * 16].contiguous()
+            kw = _epilogue_args(ep, arrays, plan.KT * 16)
             accumulate = bool(torch.any(y0 != 0))
             fuse = ep is not None and not accumulate
-            y = ops.conv2d_nchw16c(x.contiguous(), w.contiguous(),
-                                   bias if fuse else None, stride=plan.stride, pad=0,
-                                   relu=fuse and ep.relu, mode=mode)
+            y = ops.conv2d_nchw16c(x.contiguous(), w.contiguous(), stride=plan.stride, pad=0,
+                                   mode=mode, **(kw if fuse else {}))
             y = y[:, :, :plan.P, :plan.Q, :]
             if accumulate:           # `+=` onto non-zero incoming contents
-                y = y + y0
-            if ep is not None and not fuse:
-                if bias is not None:
-                    y = y + bias.reshape(1, plan.KT, 1, 1, 16)
-                if ep.relu:
-                    y = torch.where(0.0 > y, torch.zeros_like(y), y)
+                y = (y + y0).contiguous()
+                if ep is not None:   # the epilogue after the accumulation, on the GPU
+                    ops.bias_relu_(y, **kw)
             arrays[plan.out] = y.contiguous()
         elif isinstance(plan, GemmPlan):
             c0 = arrays[plan.C]
@@ -419,35 +476,30 @@ def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
             ep = plan.epilogue
             beta = 1.0 if bool(torch.any(c0 != 0)) else 0.0
             c = c0.clone() if beta else torch.empty_like(c0)
-            fuse_relu = ep is not None and ep.relu and ep.bias is None
-            ops.gemm(a, b, c, beta=beta, relu=fuse_relu, mode=mode)
-            if ep is not None and not fuse_relu:
+            # pdl_gemm_f32 fuses ReLU / ReLU6; a GEMM bias or scale has no C-ABI slot
+            fuse_act = ep is not None and ep.bias is None and ep.scale is None
+            ops.gemm(a, b, c, beta=beta, relu=fuse_act and ep.relu, relu6=fuse_act and ep.relu6,
+                     mode=mode)
+            if ep is not None and not fuse_act:
+                if ep.scale is not None:
+                    c = c * arrays[ep.scale].reshape(1, -1)[:, :plan.N]
                 if ep.bias is not None:
                     c = c + arrays[ep.bias].reshape(1, -1)[:, :plan.N]
-                if ep.relu:
+                if ep.relu or ep.relu6:
                     c = torch.where(0.0 > c, torch.zeros_like(c), c)
+                if ep.relu6:
+                    c = torch.where(6.0 < c, torch.full_like(c, 6.0), c)
             arrays[plan.C] = c
         else:  # stand-alone element-wise nest (no preceding heavy nest to fuse into)
             y = arrays[plan.target]
-            if plan.bias is not None:
-                if y.dim() == 5 and plan.bias_axes == (1, 4):
-                    b = arrays[plan.bias].reshape(-1).contiguous()
-                    y = y.contiguous()
-                    ops.bias_relu_(y, b, relu=plan.relu and not plan.relu6)
-                    if plan.relu6:
-                        y = torch.clamp(torch.where(0.0 > y, torch.zeros_like(y), y), max=6.0)
-                    arrays[plan.target] = y
-                    continue
-                raise InterpreterError(f"element-wise nest {plan.nest!r}: unsupported bias layout")
-            if y.dim() == 5:
+            if y.dim() == 5 and y.shape[-1] == 16 and plan.channel_axes_ok((1, 4)):
                 y = y.contiguous()
-                ops.bias_relu_(y, None, relu=True)
-                if plan.relu6:
-                    y = torch.clamp(y, max=6.0)
+                ops.bias_relu_(y, **_epilogue_args(plan, arrays, y.shape[1] * 16))
                 arrays[plan.target] = y
                 continue
             raise InterpreterError(f"element-wise nest {plan.nest!r} is only supported on nChw16c "
-                                   "conv outputs or fused after a GEMM")
+                                   "conv outputs (channel-indexed bias / scale) or fused after a "
+                                   "GEMM")
     if keep_on_device:
         return arrays
     return {k: v.detach().to("cpu", torch.float64).reshape(-1).numpy() for k, v in arrays.items()}

@@ -15,7 +15,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (PDL_BIAS, PDL_HOST_X_READY, PDL_OP_GEMM, PDL_RELU, MODES, TileCfg, check, lib)
+from ._lib import (PDL_BIAS, PDL_HOST_X_READY, PDL_OP_GEMM, PDL_RELU, PDL_RELU6, PDL_SCALE, MODES,
+                   TileCfg, check, lib)
 
 
 def _mode(mode: str) -> int:
@@ -109,14 +110,33 @@ def prepack_weights(w: torch.Tensor, mode: str = "3xtf32", channels: int | None 
     return PackedWeights(out, C, K, r, s, mode.lower())
 
 
+def _epilogue(bias, relu: bool, relu6: bool, scale, K: int):
+    """Epilogue flags and the device buffer the kernels read them from: `bias`
+    alone, or [shift[K] | scale[K]] when a per-channel scale is fused (PDL_SCALE)."""
+    _need_cuda_f32("bias", bias)
+    _need_cuda_f32("scale", scale)
+    flags = (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0) | \
+        (PDL_RELU6 if relu6 else 0)
+    buf = bias
+    if scale is not None:
+        if scale.numel() != K or (bias is not None and bias.numel() != K):
+            raise ValueError(f"scale / bias must hold K={K} values")
+        shift = bias.reshape(-1) if bias is not None else torch.zeros(K, device=scale.device)
+        buf = torch.cat([shift, scale.reshape(-1)])
+        flags |= PDL_SCALE
+    return flags, buf
+
+
 def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride: int = 1,
                    pad: int = 0, relu: bool = False, mode: str = "3xtf32", cfg=None,
                    out: torch.Tensor | None = None, channels: int | None = None,
-                   stream=None) -> torch.Tensor:
-    """Blocked conv fwd (+bias, +ReLU fused in the epilogue).  `w` is either raw
-    KCRS16c16k weights or a PackedWeights from prepack_weights().  `channels` =
-    true input channels when x's last 16-channel block is zero-padded (C <= 4
-    selects the narrow stem kernel)."""
+                   stream=None, relu6: bool = False, scale: torch.Tensor | None = None) -> torch.Tensor:
+    """Blocked conv fwd with the fused epilogue y = act(conv * scale[k] + bias[k]),
+    act = ReLU (relu=True) or ReLU6 (relu6=True); scale (batch-norm inference
+    affine) and bias optional.  `w` is either raw KCRS16c16k weights or a
+    PackedWeights from prepack_weights().  `channels` = true input channels when
+    x's last 16-channel block is zero-padded (C <= 4 selects the narrow stem
+    kernel)."""
     _need_cuda_f32("x", x)
     _need_cuda_f32("bias", bias)
     n, ct, h, wd, v = x.shape
@@ -139,7 +159,8 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
     y = out if out is not None else torch.empty((n, K // 16, P, Q, 16), dtype=torch.float32,
                                                 device=x.device)
     _need_cuda_f32("out", y)
-    flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    eflags, bias = _epilogue(bias, relu, relu6, scale, K)
+    flags = _mode(mode) | eflags
     st = ctypes.c_void_p(_stream(stream))
     cp = _cfg_ptr(cfg)
     if packed is not None:
@@ -180,7 +201,8 @@ def _host_workspace(device, stream_handle: int, nbytes: int) -> torch.Tensor:
 def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | None = None,
                         stride: int = 1, pad: int = 0, relu: bool = False, mode: str = "3xtf32",
                         cfg=None, out: torch.Tensor | None = None, chunk: int = 0,
-                        device=None, stream=None, x_ready: bool = False) -> torch.Tensor:
+                        device=None, stream=None, x_ready: bool = False, relu6: bool = False,
+                        scale: torch.Tensor | None = None) -> torch.Tensor:
     """Blocked conv fwd over HOST buffers (the reference's interpret() contract:
     host arrays in, host array out).  x / out are CPU float32 tensors -- pinned
     for full PCIe speed -- weights (PackedWeights) and bias live on the GPU.  The
@@ -210,7 +232,8 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     need = lib().pdl_conv2d_host_workspace_bytes(n, w.C, w.K, h, wd, w.R, w.S, stride, pad, chunk)
     sh = _stream(stream)
     ws = _host_workspace(dev, sh, need)
-    flags = _mode(mode) | (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    eflags, bias = _epilogue(bias, relu, relu6, scale, w.K)
+    flags = _mode(mode) | eflags
     if x_ready:
         flags |= PDL_HOST_X_READY
     check(lib().pdl_conv2d_fwd_host(_ptr(x), _ptr(w.data), _ptr(bias), _ptr(y), n, w.C, w.K, h, wd,
@@ -221,8 +244,8 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha: float = 1.0,
          beta: float = 0.0, relu: bool = False, mode: str = "3xtf32", cfg=None,
-         stream=None) -> torch.Tensor:
-    """C = alpha * A @ B + beta * C (row-major fp32)."""
+         stream=None, relu6: bool = False) -> torch.Tensor:
+    """C = act(alpha * A @ B + beta * C) (row-major fp32), act = ReLU / ReLU6 / none."""
     for nm, t in (("a", a), ("b", b)):
         _need_cuda_f32(nm, t)
     m, k = a.shape
@@ -234,7 +257,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha:
             raise ValueError("beta != 0 needs c")
         c = torch.empty((m, n), dtype=torch.float32, device=a.device)
     _need_cuda_f32("c", c)
-    flags = _mode(mode) | (PDL_RELU if relu else 0)
+    flags = _mode(mode) | (PDL_RELU if relu else 0) | (PDL_RELU6 if relu6 else 0)
     cp = _cfg_ptr(cfg)
     sh = _stream(stream)
     dims = (ctypes.c_int * 4)(m, n, k, flags)
@@ -246,12 +269,12 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha:
 
 
 def bias_relu_(y: torch.Tensor, bias: torch.Tensor | None, relu: bool = True,
-               stream=None) -> torch.Tensor:
-    """Unfused element-wise pass y = max(y + bias, 0) in place (GPU baseline)."""
+               stream=None, relu6: bool = False, scale: torch.Tensor | None = None) -> torch.Tensor:
+    """Unfused element-wise pass y = act(y * scale + bias) in place over nKhw16k (the
+    GPU baseline of the fused epilogue, and the stand-alone element-wise nest)."""
     _need_cuda_f32("y", y)
-    _need_cuda_f32("bias", bias)
     n, kt, p, q, v = y.shape
-    flags = (PDL_BIAS if bias is not None else 0) | (PDL_RELU if relu else 0)
+    flags, bias = _epilogue(bias, relu, relu6, scale, kt * 16)
     check(lib().pdl_bias_relu_nchw16c(_ptr(y), _ptr(bias), n, kt * 16, p, q, flags,
                                       ctypes.c_void_p(_stream(stream))))
     return y

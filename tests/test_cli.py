@@ -59,8 +59,13 @@ def test_emit_fuse_train(conv_relu, tmp_path, capsys):
     assert json.loads(capsys.readouterr().out)["launch"]["bn"] == 64
     assert main(["emit", conv_relu, "--bind", CONV_BIND, "--variant", "nope"]) == 1
     assert main(["fuse", conv_relu, "--bind", CONV_BIND]) == 0
-    plans = json.loads(capsys.readouterr().out)["plans"]
+    rep = json.loads(capsys.readouterr().out)
+    plans = rep["plans"]
     assert plans[0]["kind"] == "conv" and plans[0]["fused_epilogue"]["relu"]
+    assert rep["decision"]["fusable"] and "Sc_p1" in rep["fused_pdl"]
+    assert main(["fuse", conv_relu, "--bind", CONV_BIND, "--emit-pdl", str(tmp_path / "f.pdl")]) == 0
+    capsys.readouterr()
+    assert (tmp_path / "f.pdl").read_text() == rep["fused_pdl"]
     rows = [(rank.VariantStats("a", 1, 2, 3, 4), rank.VariantStats("b", 4, 3, 2, 1), 0)] * 8
     rank.save_dataset(str(tmp_path / "d.csv"), rows)
     assert main(["train", str(tmp_path / "d.csv"), "--out", str(tmp_path / "m.npz"),
