@@ -187,7 +187,7 @@ def cpu_suite_sample(layers, seconds_budget: float, threads: int):
     flops = sum(l.flops(1) for l in layers)
     cpu_step(prepared, threads)  # page-in
     t_total, reps = 0.0, 0
-    while reps == 0 or (t_total < seconds_budget and reps < 50):
+    while reps == 0 or (t_total < seconds_budget and reps < 1000):
         t0 = time.perf_counter()
         cpu_step(prepared, threads)
         t_total += time.perf_counter() - t0
