@@ -85,9 +85,10 @@ enum {
     PDL_MODE_TF32 = 1 << 4,
     PDL_MODE_FP32 = 2 << 4,
     PDL_MODE_MASK = 3 << 4,
-    PDL_HOST_X_READY = 1 << 6 /* pdl_conv2d_fwd_host: x_host is final at call time (not
-                                 written by work still pending on the stream), so its
-                                 copies may overlap an earlier call's copies out     */
+    PDL_HOST_X_READY = 1 << 6 /* pdl_conv2d_fwd_host: x_host, packed_w and bias are
+                                 final at call time (not written by work still pending
+                                 on the stream), so this call's copies in and
+                                 convolutions may overlap an earlier call's copies out */
 };
 
 enum {
@@ -147,11 +148,13 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
  * chunk's host->device copy, convolution (on `stream`) and device->host copy
  * run on separate streams through 3 staging slots, so both PCIe directions and
  * the tensor cores overlap.  Ordered after prior work on `stream` (with
- * PDL_HOST_X_READY in flags only the device side is: the copies in may start
- * while an earlier call's copies out are still running); work enqueued on
- * `stream` after the call sees y_host complete.  workspace must hold
- * pdl_conv2d_host_workspace_bytes(...) bytes (same chunk): an x half written by
- * copies in and a y half read by copies out. */
+ * PDL_HOST_X_READY in flags and the same workspace as the previous call, only
+ * after that call's convolutions: the copies in and convolutions may run while
+ * its copies out are still going); work enqueued on `stream` after the call sees
+ * y_host complete.  workspace must hold pdl_conv2d_host_workspace_bytes(...)
+ * bytes (same chunk): an x third written by copies in (3 chunk slots) and two y
+ * thirds (each the call's whole output) read by copies out, used by alternate
+ * calls. */
 size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R, int S,
                                        int stride, int pad, int chunk);
 int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *bias,

@@ -825,10 +825,12 @@ constexpr int kHostSlots = 3;     // device staging slots (x and y) in flight
 constexpr int kMaxDevices = 16;
 struct HostPipe {
     bool ready = false;
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t entry = nullptr, x_in[kHostSlots], done[kHostSlots], y_out[kHostSlots];
+    cudaStream_t h2d = nullptr, d2h = nullptr, cs = nullptr;  // copies in / out, convolutions
+    cudaEvent_t entry = nullptr, x_in[kHostSlots], done[kHostSlots], y_done[2];
     cudaEvent_t x_free = nullptr;     // last conv of the previous call (x area no longer read)
     const void *last_ws = nullptr;    // workspace of the previous call
+    size_t last_ws_bytes = 0;
+    int parity = 0;                   // y area half of the next call
 };
 thread_local HostPipe g_pipe[kMaxDevices];
 
@@ -841,12 +843,15 @@ int host_pipe(HostPipe **out) {
         const unsigned ef = cudaEventDisableTiming;
         bool ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&hp.cs, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaEventCreateWithFlags(&hp.entry, ef) == cudaSuccess &&
                   cudaEventCreateWithFlags(&hp.x_free, ef) == cudaSuccess;
         for (int i = 0; ok && i < kHostSlots; ++i)
             ok = cudaEventCreateWithFlags(&hp.x_in[i], ef) == cudaSuccess &&
-                 cudaEventCreateWithFlags(&hp.done[i], ef) == cudaSuccess &&
-                 cudaEventCreateWithFlags(&hp.y_out[i], ef) == cudaSuccess;
+                 cudaEventCreateWithFlags(&hp.done[i], ef) == cudaSuccess;
+        for (int q = 0; ok && q < 2; ++q)
+            ok = cudaEventCreateWithFlags(&hp.y_done[q], ef) == cudaSuccess &&
+                 cudaEventRecord(hp.y_done[q], hp.d2h) == cudaSuccess;
         if (!ok) return fail(PDL_ELAUNCH, "conv host: stream/event creation failed");
         hp.ready = true;
     }
@@ -960,9 +965,11 @@ size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R,
     if (P <= 0 || Q <= 0) return 0;
     const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
     const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
-    // [x area | y area], equal halves: copies in only write the x area and copies out
-    // only read the y area, so a call's H2D never waits for an earlier call's D2H
-    return 2 * align256((size_t)kHostSlots * std::max(align256(c * x_img), align256(c * y_img)));
+    // [x area | y area 0 | y area 1], equal thirds: copies in only write the x area (3 chunk
+    // slots), a y area holds the call's whole output (the convolutions never wait for copies
+    // out), and consecutive calls alternate y areas, so a call's H2D and convolutions never
+    // wait for the previous call's D2H
+    return 3 * align256(std::max((size_t)kHostSlots * align256(c * x_img), (size_t)N * y_img));
 }
 
 int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *bias,
@@ -992,58 +999,69 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
     const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
     const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
-    const size_t xs = align256(c * x_img), ys = align256(c * y_img);
+    const size_t xs = align256(c * x_img);
     uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
-    uint8_t *ws_y = ws + (ws_bytes / 2 & ~(size_t)255);  // y area: second half
+    const size_t third = ws_bytes / 3 & ~(size_t)255;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned cflags = flags & ~(unsigned)PDL_HOST_X_READY;
-    // chunk i uses slot i % kHostSlots:
+    // Three internal streams; chunk i uses x slot i % kHostSlots and its own images' place
+    // in this call's y area q (the whole output):
     //   h2d: [slot's previous conv done] copy x  -> x_in
-    //   st : [x_in, slot's previous y copy done] conv -> done
-    //   d2h: [done] copy y -> y_out
-    // entry orders the first use of every slot after prior work on `stream`.  With
-    // PDL_HOST_X_READY (x_host is final now) and the workspace of the previous call, the
-    // copies in only wait for that call's convolutions to release the x area, so they
-    // overlap the previous call's copies out (consecutive layers pipeline end to end).
+    //   cs : [x_in] conv -> done
+    //   d2h: [done] copy y;  after the last chunk -> y_done[q]
+    // Default: everything is ordered after prior work on `stream` (entry event).  With
+    // PDL_HOST_X_READY (x_host, packed_w and bias are final at call time) and the
+    // workspace of the previous call, the copies in only wait for that call's last
+    // convolution to release the x area and the convolutions only for their own y area
+    // (the previous call used the other one), so the previous call's copies out overlap
+    // this call's copies in AND convolutions: both PCIe directions stay busy across layers.
+    // `stream` waits for this call's copies out before any later work.
     if (cudaEventRecord(hp->entry, st) != cudaSuccess)
         return fail(PDL_ELAUNCH, "conv host: entry event");
-    const bool relaxed = (flags & PDL_HOST_X_READY) && hp->last_ws == workspace;
-    if (cudaStreamWaitEvent(hp->h2d, relaxed ? hp->x_free : hp->entry, 0) != cudaSuccess)
+    const bool relaxed = (flags & PDL_HOST_X_READY) && hp->last_ws == workspace && hp->last_ws_bytes == ws_bytes;
+    if (!relaxed) hp->parity = 0;
+    const int q = hp->parity;
+    uint8_t *ws_y = ws + (size_t)(1 + q) * third;
+    if (cudaStreamWaitEvent(hp->h2d, relaxed ? hp->x_free : hp->entry, 0) != cudaSuccess ||
+        (!relaxed && cudaStreamWaitEvent(hp->cs, hp->entry, 0) != cudaSuccess))
         return fail(PDL_ELAUNCH, "conv host: entry wait");
+    // this y area's previous user (two calls back) must have copied all of it out
+    if (cudaStreamWaitEvent(hp->cs, hp->y_done[q], 0) != cudaSuccess)
+        return fail(PDL_ELAUNCH, "conv host: y area wait");
     const int nchunks = (N + c - 1) / c;
     int launches = 0;
     for (int i = 0; i < nchunks; ++i) {
         const int b = i % kHostSlots;
         const int n0 = i * c, n = std::min(c, N - n0);
         float *xd = reinterpret_cast<float *>(ws + b * xs);
-        float *yd = reinterpret_cast<float *>(ws_y + b * ys);
+        float *yd = reinterpret_cast<float *>(ws_y + n0 * y_img);
         if (i >= kHostSlots && cudaStreamWaitEvent(hp->h2d, hp->done[b], 0) != cudaSuccess)
             return fail(PDL_ELAUNCH, "conv host: wait");
         if (cudaMemcpyAsync(xd, reinterpret_cast<const uint8_t *>(x_host) + n0 * x_img, n * x_img,
                             cudaMemcpyHostToDevice, hp->h2d) != cudaSuccess ||
             cudaEventRecord(hp->x_in[b], hp->h2d) != cudaSuccess)
             return fail(PDL_ELAUNCH, "conv host: H2D copy: %s", cudaGetErrorString(cudaGetLastError()));
-        if (cudaStreamWaitEvent(st, hp->x_in[b], 0) != cudaSuccess ||
-            (i >= kHostSlots && cudaStreamWaitEvent(st, hp->y_out[b], 0) != cudaSuccess))
+        if (cudaStreamWaitEvent(hp->cs, hp->x_in[b], 0) != cudaSuccess)
             return fail(PDL_ELAUNCH, "conv host: wait");
         if ((rc = conv_fwd_tc(xd, reinterpret_cast<const float *>(packed_w), bias, yd, n, C, K, H, W,
-                              R, S, stride, pad, cflags, cfg, st)))
+                              R, S, stride, pad, cflags, cfg, hp->cs)))
             return rc;
         launches += g_launches;
-        if (cudaEventRecord(hp->done[b], st) != cudaSuccess ||
+        if (cudaEventRecord(hp->done[b], hp->cs) != cudaSuccess ||
             cudaStreamWaitEvent(hp->d2h, hp->done[b], 0) != cudaSuccess ||
             cudaMemcpyAsync(reinterpret_cast<uint8_t *>(y_host) + n0 * y_img, yd, n * y_img,
-                            cudaMemcpyDeviceToHost, hp->d2h) != cudaSuccess ||
-            cudaEventRecord(hp->y_out[b], hp->d2h) != cudaSuccess)
+                            cudaMemcpyDeviceToHost, hp->d2h) != cudaSuccess)
             return fail(PDL_ELAUNCH, "conv host: D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
     }
     // the x area is free once the last convolution has run (next call's copies in)
-    if (cudaEventRecord(hp->x_free, st) != cudaSuccess) return fail(PDL_ELAUNCH, "conv host: x_free");
+    if (cudaEventRecord(hp->x_free, hp->cs) != cudaSuccess) return fail(PDL_ELAUNCH, "conv host: x_free");
     hp->last_ws = workspace;
-    // later work on `stream` (and the next call's slot reuse) sees every y copy done
-    for (int b = 0; b < std::min(nchunks, kHostSlots); ++b)
-        if (cudaStreamWaitEvent(st, hp->y_out[b], 0) != cudaSuccess)
-            return fail(PDL_ELAUNCH, "conv host: exit wait");
+    hp->last_ws_bytes = ws_bytes;
+    hp->parity = q ^ 1;
+    // later work on `stream` sees every y copy (and so every convolution) done
+    if (cudaEventRecord(hp->y_done[q], hp->d2h) != cudaSuccess ||
+        cudaStreamWaitEvent(st, hp->y_done[q], 0) != cudaSuccess)
+        return fail(PDL_ELAUNCH, "conv host: exit wait");
     g_launches = launches;
     return PDL_OK;
 }

@@ -209,9 +209,10 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     library pipelines image chunks: H2D copy, fused conv and D2H copy overlap
     (pdl_conv2d_fwd_host).  Returns `out` (allocated pinned if None), complete
     once `stream` reaches the point after this call.  x_ready=True promises that
-    x is not written by work still pending on `stream` (e.g. it is not the output
-    of an earlier host call): its copies in may then overlap the previous call's
-    copies out (PDL_HOST_X_READY)."""
+    x, the packed weights and bias are not written by work still pending on
+    `stream` (e.g. x is not the output of an earlier host call): this call's
+    copies in and convolutions may then overlap the previous call's copies out
+    (PDL_HOST_X_READY)."""
     if not isinstance(w, PackedWeights):
         raise TypeError("conv2d_nchw16c_host takes PackedWeights (prepack_weights())")
     if not isinstance(x, torch.Tensor) or x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
@@ -234,7 +235,7 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     ws = _host_workspace(dev, sh, need)
     eflags, bias = _epilogue(bias, relu, relu6, scale, w.K)
     flags = _mode(mode) | eflags
-    if x_ready:
+    if x_ready and scale is None:   # (a fused scale builds its [shift | scale] buffer on `stream`)
         flags |= PDL_HOST_X_READY
     check(lib().pdl_conv2d_fwd_host(_ptr(x), _ptr(w.data), _ptr(bias), _ptr(y), n, w.C, w.K, h, wd,
                                     w.R, w.S, stride, pad, flags, _cfg_ptr(cfg), int(chunk),
