@@ -17,7 +17,8 @@ for idx in idxs:
     pw = P.prepack_weights(w, channels=l.C)
     y = torch.empty((n, l.K // 16, l.P, l.Q, 16), device='cuda')
     menu = [("auto", None), ("s1", {"split_k": 1}), ("s2", {"split_k": 2}), ("s3", {"split_k": 3}),
-            ("s4", {"split_k": 4}), ("bn64", {"bn": 64}), ("bn64_s1", {"bn": 64, "split_k": 1}),
+            ("s4", {"split_k": 4}), ("s6", {"split_k": 6}), ("s8", {"split_k": 8}),
+            ("bn64", {"bn": 64}), ("bn64_s1", {"bn": 64, "split_k": 1}),
             ("bn64_s2", {"bn": 64, "split_k": 2})]
     res = []
     for name, cfg in menu:
