@@ -127,7 +127,7 @@ def test_host_path_fused_epilogue_equals_device(P):
     assert torch.equal(dev.cpu(), host)
 
 
-@pytest.mark.parametrize("shape", [(256, 192, 320), (96, 64, 33)])
+@pytest.mark.parametrize("shape", [(256, 192, 320), (96, 64, 33), (128, 128, 4096), (64, 256, 2048)])
 def test_gemm_relu6(P, shape):
     m, n, k = shape
     rng = np.random.default_rng(m)
@@ -146,3 +146,23 @@ def test_scale_needs_k_values(P):
     w = torch.zeros((2, 1, 1, 1, 16, 16), device="cuda")
     with pytest.raises(ValueError):
         P.conv2d_nchw16c(x, w, scale=torch.ones(16, device="cuda"))
+
+
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("split_k", [2, 3])
+def test_split_k_reduction_applies_extended_epilogue_once(P, mode, split_k):
+    """Scale + bias + ReLU6 on the split-K path: partials are written raw, the last
+    unit of each tile applies the epilogue once (layer 17 at 2 images: 8 tiles)."""
+    layer = W.LAYERS[17 - 1]
+    x, w, b = W.conv_inputs(layer, 2, seed=77)
+    s = np.random.default_rng(1).uniform(0.5, 8.0, layer.K).astype(np.float32)
+    pw = P.prepack_weights(torch.from_numpy(w).cuda(), mode=mode)
+    X, bd, sd = (torch.from_numpy(t).cuda() for t in (x, b, s))
+    kw = dict(stride=layer.stride, pad=layer.pad, mode=mode, relu6=True, scale=sd)
+    y = P.conv2d_nchw16c(X, pw, bd, cfg={"split_k": split_k}, **kw)
+    y1 = P.conv2d_nchw16c(X, pw, bd, cfg={"split_k": 1}, **kw)
+    conv = oracle.conv2d_f64(x, w, None, stride=layer.stride, pad=layer.pad)
+    pre = epi_ref(conv, b, s)
+    ref = epi_ref(conv, b, s, "relu6")
+    for out in (y, y1):
+        assert np.abs(out.cpu().numpy() - ref).max() / np.abs(pre).max() <= TOL[mode]
