@@ -1179,7 +1179,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (tr) trace_ev(p, TR_E_DRAINED, g);
             }
             if (SPL > 1) {
-                // ---- split-K: publish this unit's partial; the tile's last unit reduces
+                // ---- split-K: publish this unit's partial; the tile's last unit reduces.
+                // (A fixed reducer per tile, sp == tile % SPL, was tried: its waits for late
+                // parts cost what spreading the reductions saved -- L18 at 32 images, 4-way
+                // split: 122.9 us vs 122.1 with this rule -- so the simpler rule stays.
+                // Splits pay only for long ranges; plan_split asks for >= 16 k-blocks.)
                 const int tile = tile_of(st_i);
                 float *mine = p.part + ((size_t)tile * SPL + sp) * (128 * BN);
 #pragma unroll
@@ -1202,27 +1206,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!*split_flag) continue;
                 __threadfence();
                 // fixed split order (independent of arrival order): ((p0 + p1) + p2) + ...;
-                // this unit's own partial is read back too (registers stay free)
+                // this unit's own partial is read back too (registers stay free).  Loads are
+                // batched (all of p0, then 8 float4 of each later partial at a time): one
+                // dependent L2 round trip per batch, not per 16 columns and partial (L18 at
+                // 32 images: 4-way split 131.8 -> 122.1 us, 8-way 530 -> 432 us)
                 const float *tp = p.part + (size_t)tile * SPL * (128 * BN);
+                auto poff = [&](int j) { return ((half * (HALF / 16) + j) * 128 + row) * 16; };
 #pragma unroll
-                for (int j = 0; j < HALF / 16; ++j) {
-                    const int off = ((half * (HALF / 16) + j) * 128 + row) * 16;
-                    float4 t[4];
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) t[q4] = __ldcg(reinterpret_cast<const float4 *>(tp + off) + q4);
-#pragma unroll 1
-                    for (int q = 1; q < SPL; ++q) {
-                        const float4 *src = reinterpret_cast<const float4 *>(tp + (size_t)q * (128 * BN) + off);
-#pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
-                            const float4 w4 = __ldcg(src + q4);
-                            t[q4].x += w4.x; t[q4].y += w4.y; t[q4].z += w4.z; t[q4].w += w4.w;
-                        }
-                    }
+                for (int j = 0; j < HALF / 16; ++j)
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
-                        sum[j * 16 + q4 * 4] = t[q4].x; sum[j * 16 + q4 * 4 + 1] = t[q4].y;
-                        sum[j * 16 + q4 * 4 + 2] = t[q4].z; sum[j * 16 + q4 * 4 + 3] = t[q4].w;
+                        const float4 v4 = __ldcg(reinterpret_cast<const float4 *>(tp + poff(j)) + q4);
+                        sum[j * 16 + q4 * 4] = v4.x; sum[j * 16 + q4 * 4 + 1] = v4.y;
+                        sum[j * 16 + q4 * 4 + 2] = v4.z; sum[j * 16 + q4 * 4 + 3] = v4.w;
+                    }
+#pragma unroll 1
+                for (int q = 1; q < SPL; ++q) {
+                    const float *src = tp + (size_t)q * (128 * BN);
+#pragma unroll
+                    for (int j0 = 0; j0 < HALF / 16; j0 += 2) {
+                        float4 w4[2][4];
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4)
+                                w4[jj][q4] = (j0 + jj < HALF / 16)
+                                                 ? __ldcg(reinterpret_cast<const float4 *>(src + poff(j0 + jj)) + q4)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj) {
+                            if (j0 + jj >= HALF / 16) break;
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) {
+                                float *d = &sum[(j0 + jj) * 16 + q4 * 4];
+                                d[0] += w4[jj][q4].x; d[1] += w4[jj][q4].y;
+                                d[2] += w4[jj][q4].z; d[3] += w4[jj][q4].w;
+                            }
+                        }
                     }
                 }
             }
