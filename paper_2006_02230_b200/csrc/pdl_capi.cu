@@ -859,10 +859,15 @@ int host_pipe(HostPipe **out) {
     return PDL_OK;
 }
 
-// Images per pipeline chunk: ~16 MB of x per copy (PCIe-efficient transfers), at
+// x bytes per host-pipeline copy.  e2e A/B on the 256-image suite (scripts/ab_e2e.sh,
+// profiles/e2e_chunk_ab_r1o.log): 8 MB 138.8 ms/step, 16 MB 130.8, 32 MB 127.6, 64 MB 126.8
+#ifndef PDL_HOST_CHUNK_MB
+#define PDL_HOST_CHUNK_MB 64
+#endif
+// Images per pipeline chunk: ~64 MB of x per copy (PCIe-efficient transfers), at
 // least 4 chunks when the batch allows (so both copy directions overlap).
 int host_chunk(int N, size_t x_img) {
-    const size_t target = (size_t)16 << 20;
+    const size_t target = (size_t)PDL_HOST_CHUNK_MB << 20;
     int c = (int)std::max<size_t>(1, target / std::max<size_t>(x_img, 1));
     return std::max(1, std::min(c, (N + 3) / 4));
 }
