@@ -697,7 +697,9 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     std::memset(&maps, 0, sizeof(maps));
     // halo mode (3xTF32, stride 1, spatial filter): one box of the tile's whole input halo
     // per channel group instead of one box per tap
-    const bool halo_cg4 = cfg_in && (cfg_in->raster & PDL_RASTER_HALO_CG4);  // A/B: 3xTF32, 1 halo buffer
+    // 3xTF32 64-channel k-blocks at BN=64 (layer 3) take halo mode with one halo buffer:
+    // 333 vs 340 us isolated in round 1p (a tie in round 1l); PDL_RASTER_HALO_CG4 forces it
+    const bool halo_cg4 = (cfg_in && (cfg_in->raster & PDL_RASTER_HALO_CG4)) || cfg.bn == 64;
     const int halo_w = g.BW + S - 1, halo_h = g.BH + R - 1;
     // (3xTF32: not with 64-channel k-blocks -- two 64 KB halo buffers leave 2 weight stages,
     // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
