@@ -62,14 +62,13 @@ typedef struct pdl_tile_cfg {
     int raster;    /* bit 0: reserved (tile order); bit 1 (PDL_RASTER_BOX_TILES):
                       box tiles only -- no multi-image segment tiles for small maps;
                       bit 2 (PDL_RASTER_SEG_TILES): segment tiles whenever the shape
-                      allows, even if they do not remove a wave of tiles       */
+                      allows, even if they do not remove a wave of tiles; bits 4
+                      and 6 below; any other bit: PDL_EUNSUPPORTED              */
 } pdl_tile_cfg;
 
 #define PDL_RASTER_BOX_TILES 2
 #define PDL_RASTER_SEG_TILES 4
-#define PDL_RASTER_LSU_EPI 8   /* conv epilogue: coalesced st.global instead of TMA box stores */
 #define PDL_RASTER_NO_HALO 16  /* 3x3 convs: one A box per tap instead of one halo per channel group */
-#define PDL_RASTER_BLO_ONCHIP 32 /* halo 3xTF32 convs: load the weights' hi plane, form lo on chip */
 #define PDL_RASTER_HALO_CG4 64 /* 3xTF32 halo mode with 64-channel k-blocks (one halo buffer) */
 
 enum {
@@ -85,11 +84,17 @@ enum {
     PDL_MODE_TF32 = 1 << 4,
     PDL_MODE_FP32 = 2 << 4,
     PDL_MODE_MASK = 3 << 4,
-    PDL_HOST_X_READY = 1 << 6 /* pdl_conv2d_fwd_host: x_host, packed_w and bias are
+    PDL_HOST_X_READY = 1 << 6,/* pdl_conv2d_fwd_host: x_host, packed_w and bias are
                                  final at call time (not written by work still pending
-                                 on the stream), so this call's copies in and
-                                 convolutions may overlap an earlier call's copies out */
+                                 on the stream) and y_host is not read by such work, so
+                                 this call's copies in and convolutions may overlap an
+                                 earlier call's copies out                      */
+    PDL_NO_SIMT = 1 << 7      /* GEMM: fail with PDL_EUNSUPPORTED instead of running
+                                 the CUDA-core kernel when the operands cannot take the
+                                 tensor-core path (unaligned pointers, K = 0, or N /
+                                 lda / ldb / ldc not multiples of 4)            */
 };
+/* Every entry point rejects flag bits it does not implement (PDL_EUNSUPPORTED). */
 
 enum {
     PDL_OK = 0,
@@ -144,14 +149,17 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
  * x_host [N][C/16][H][W][16] and y_host [N][K/16][P][Q][16] are HOST pointers
  * (pinned -- cudaHostAlloc / cudaHostRegister -- or the copies serialise);
  * packed_w / bias / workspace are device pointers.  The minibatch is cut into
- * chunks of `chunk` images (0 = library default, ~16 MB of x per chunk); each
- * chunk's host->device copy, convolution (on `stream`) and device->host copy
- * run on separate streams through 3 staging slots, so both PCIe directions and
- * the tensor cores overlap.  Ordered after prior work on `stream` (with
- * PDL_HOST_X_READY in flags and the same workspace as the previous call, only
+ * chunks of `chunk` images (0 = library default, ~64 MB of x per chunk, at
+ * least 4 chunks when the batch allows); each chunk's host->device copy,
+ * convolution and device->host copy run on three internal streams (one set per
+ * device and workspace) through 3 staging slots, so both PCIe directions and the
+ * tensor cores overlap.  Ordered after prior work on `stream`; with
+ * PDL_HOST_X_READY and a previous call on the same workspace (any thread), only
  * after that call's convolutions: the copies in and convolutions may run while
- * its copies out are still going); work enqueued on `stream` after the call sees
- * y_host complete.  workspace must hold pdl_conv2d_host_workspace_bytes(...)
+ * its copies out are still going, and the copies out are NOT ordered after other
+ * work pending on `stream` (see PDL_HOST_X_READY).  Work enqueued on `stream`
+ * after the call sees y_host complete; on an error return, `stream` still waits
+ * for whatever the call had enqueued.  workspace must hold pdl_conv2d_host_workspace_bytes(...)
  * bytes (same chunk): an x third written by copies in (3 chunk slots) and two y
  * thirds (each the call's whole output) read by copies out, used by alternate
  * calls. */
@@ -162,16 +170,36 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
                         int stride, int pad, unsigned flags, const pdl_tile_cfg *cfg, int chunk,
                         void *workspace, size_t ws_bytes, void *stream);
 
-/* C = alpha * A B + beta * C, row-major with leading dimensions lda/ldb/ldc.
- * workspace: optional split-K area (same rules as pdl_conv2d_fwd_prepacked_ws),
- * pdl_workspace_bytes(PDL_OP_GEMM, {M, N, K, flags}, cfg) bytes; NULL = no split. */
+/* C = act(alpha * A B + beta * C), row-major with leading dimensions lda/ldb/ldc;
+ * act = PDL_RELU / PDL_RELU6 / none.  workspace: optional split-K area (same rules
+ * as pdl_conv2d_fwd_prepacked_ws), pdl_workspace_bytes(PDL_OP_GEMM, {M, N, K, flags},
+ * cfg) bytes; NULL = no split.  PDL_BIAS / PDL_SCALE need pdl_gemm_f32_epilogue
+ * (EINVAL here).  Operands TMA cannot describe (see PDL_NO_SIMT) run on the CUDA
+ * cores in exact fp32. */
 int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda,
                  int ldb, int ldc, float alpha, float beta, unsigned flags,
                  const pdl_tile_cfg *cfg, void *workspace, size_t ws_bytes, void *stream);
 
+/* The GEMM with the full fused epilogue of Alg. 3 (the fused
+ * GEMM + batch-norm / bias + ReLU programs): per output column n,
+ *   C = act((alpha * A B + beta * C) * scale[n] + shift[n])
+ * bias = shift[N] (PDL_BIAS), or shift[N] then scale[N] (PDL_SCALE; the shift is
+ * added only with PDL_BIAS); 16-byte aligned device pointer, may be NULL without
+ * those flags.  Same rules as pdl_gemm_f32 otherwise. */
+int pdl_gemm_f32_epilogue(const float *A, const float *B, float *C, const float *bias, int M,
+                          int N, int K, int lda, int ldb, int ldc, float alpha, float beta,
+                          unsigned flags, const pdl_tile_cfg *cfg, void *workspace,
+                          size_t ws_bytes, void *stream);
+
 /* Unfused element-wise pass over y[N][K/16][P][Q][16] (the GPU baseline). */
 int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int Q,
                           unsigned flags, void *stream);
+
+/* `+=` onto incoming output contents (the nest's output was not zero): y = the
+ * convolution result, y0 = the incoming contents; y = act((y + y0) * scale + bias)
+ * with the same flags / bias layout as the fused epilogue. */
+int pdl_accumulate_epilogue_nchw16c(float *y, const float *y0, const float *bias, int N, int K,
+                                    int P, int Q, unsigned flags, void *stream);
 
 /* Layout conversion on either side of the path (device to device):
  *   NCHW [N][C][H][W]      <-> nChw16c [N][ceil(C/16)][H][W][16] (pad channels zero)

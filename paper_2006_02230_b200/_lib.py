@@ -22,6 +22,7 @@ PDL_MODE_TF32 = 1 << 4
 PDL_MODE_FP32 = 2 << 4
 PDL_MODE_MASK = 3 << 4
 PDL_HOST_X_READY = 1 << 6
+PDL_NO_SIMT = 1 << 7
 PDL_OP_CONV2D = 1
 PDL_OP_GEMM = 2
 
@@ -37,7 +38,8 @@ EXPORTS = (
     "pdl_workspace_bytes", "pdl_default_cfg", "pdl_last_launch_count", "pdl_last_error",
     "pdl_abi_version", "pdl_device_check", "pdl_pack_nchw16c", "pdl_unpack_nchw16c",
     "pdl_pack_kcrs16c16k", "pdl_conv2d_host_workspace_bytes", "pdl_conv2d_fwd_host",
-    "pdl_conv2d_splitk_workspace_bytes", "pdl_conv2d_fwd_prepacked_ws",
+    "pdl_conv2d_splitk_workspace_bytes", "pdl_conv2d_fwd_prepacked_ws", "pdl_gemm_f32_epilogue",
+    "pdl_accumulate_epilogue_nchw16c",
 )
 
 
@@ -99,7 +101,10 @@ def _declare(L):
         _u, ctypes.POINTER(TileCfg), _i, _vp, _sz, _vp]
     L.pdl_gemm_f32.argtypes = [_vp, _vp, _vp] + [_i] * 6 + [
         ctypes.c_float, ctypes.c_float, _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
+    L.pdl_gemm_f32_epilogue.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 6 + [
+        ctypes.c_float, ctypes.c_float, _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
     L.pdl_bias_relu_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
+    L.pdl_accumulate_epilogue_nchw16c.argtypes = [_vp, _vp, _vp, _i, _i, _i, _i, _u, _vp]
     L.pdl_pack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_unpack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_pack_kcrs16c16k.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -70,20 +71,47 @@ int encode(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims,
 }
 
 // ---------------------------------------------------------------- device check
-int g_dev_ok = -1;
-std::once_flag g_dev_once;
-int sm_count = 148;
+// Per-device state (a process may drive several GPUs, e.g. one host thread per
+// device): the sm_100 check and the SM count, each initialised once per device.
+constexpr int kMaxDevices = 16;
+struct DevInfo {
+    std::once_flag once;
+    int ok = 0;
+    int sms = 148;
+};
+DevInfo g_dev[kMaxDevices];
 
-int device_check() {
-    std::call_once(g_dev_once, [] {
-        int dev = 0, major = 0, minor = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) { g_dev_ok = 0; return; }
+int cur_dev() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+    return dev;
+}
+
+DevInfo *dev_info() {
+    const int dev = cur_dev();
+    if (dev < 0) return nullptr;
+    DevInfo &d = g_dev[dev];
+    std::call_once(d.once, [&] {
+        int major = 0, minor = 0, sms = 0;
         cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
         cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-        g_dev_ok = (major == 10 && minor == 0) ? 1 : 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+            d.sms = sms;
+        d.ok = (major == 10 && minor == 0) ? 1 : 0;
+        cudaGetLastError();
     });
-    if (g_dev_ok != 1) return fail(PDL_EDEVICE, "libpdl requires an sm_100 (B200) device");
+    return &d;
+}
+
+// SM count of the current device (148 on B200; the planners size grids by it)
+int sms() {
+    const DevInfo *d = dev_info();
+    return d ? d->sms : 148;
+}
+
+int device_check() {
+    const DevInfo *d = dev_info();
+    if (!d || d->ok != 1) return fail(PDL_EDEVICE, "libpdl requires an sm_100 (B200) device");
     return PDL_OK;
 }
 
@@ -107,6 +135,25 @@ constexpr int kDefaultConvCluster = 1;
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Flag bits each entry point accepts; anything else is rejected rather than ignored.
+// The diagnostic bits (pdl::kDiagBits) exist only in -DPDL_DIAG builds.
+#ifdef PDL_DIAG
+constexpr unsigned kDiag = pdl::kDiagBits;
+#else
+constexpr unsigned kDiag = 0;
+#endif
+constexpr unsigned kEpiFlags = PDL_BIAS | PDL_RELU | PDL_RELU6 | PDL_SCALE;
+constexpr unsigned kConvFlags = kEpiFlags | PDL_MODE_MASK;
+constexpr unsigned kGemmFlags = kEpiFlags | PDL_MODE_MASK | PDL_NO_SIMT;
+constexpr int kRasterBits = 1 | PDL_RASTER_BOX_TILES | PDL_RASTER_SEG_TILES | PDL_RASTER_NO_HALO | PDL_RASTER_HALO_CG4;
+
+int check_flags(unsigned flags, unsigned allowed, const char *what) {
+    const unsigned bad = flags & ~(allowed | kDiag);
+    if (bad) return fail(PDL_EUNSUPPORTED, "%s: unsupported flag bits 0x%x", what, bad);
+    if ((flags & PDL_MODE_MASK) == PDL_MODE_MASK) return fail(PDL_EINVAL, "%s: invalid mode bits", what);
+    return PDL_OK;
+}
+
 // ---------------------------------------------------------------- launch helpers
 // Persistent launch: grid = as many CTAs (clusters of CL) as can be co-resident,
 // capped by the work.  Clusters of 4 cannot use every SM (GPC granularity), so
@@ -116,9 +163,13 @@ template <int KIND, int BN, int CG, bool SPLIT3, int CL, bool PAIR = false, int 
 int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_ctas, cudaStream_t s) {
     using L = pdl::Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
     auto kern = pdl::tile_mma_kernel<KIND, BN, CG, SPLIT3, CL, PAIR, RESW, HALO, EPIX>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    static int max_ctas = 0;
+    // the dynamic-smem attribute and the co-resident CTA count are per device
+    static std::once_flag once[kMaxDevices];
+    static cudaError_t attr_err[kMaxDevices];
+    static int max_ctas[kMaxDevices];
+    const int dev = cur_dev();
+    if (dev < 0) return fail(PDL_EDEVICE, "tile_mma_kernel: no current device");
+    const int sm_count = sms();
     cudaLaunchConfig_t lc = {};
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -135,19 +186,19 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
     lc.stream = s;
     lc.attrs = at;
     lc.numAttrs = 2;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-        if (attr_err != cudaSuccess) return;
+    std::call_once(once[dev], [&] {
+        attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        if (attr_err[dev] != cudaSuccess) return;
         int ncl = 0;
         lc.gridDim = dim3(CL * 64);
         if (cudaOccupancyMaxActiveClusters(&ncl, kern, &lc) != cudaSuccess || ncl <= 0)
             ncl = sm_count / CL;
         cudaGetLastError();
-        max_ctas = std::min(ncl * CL, sm_count / CL * CL);
+        max_ctas[dev] = std::min(ncl * CL, sm_count / CL * CL);
     });
-    if (attr_err != cudaSuccess)
-        return fail(PDL_ELAUNCH, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-    int grid = std::min(max_ctas, (work_ctas + CL - 1) / CL * CL);
+    if (attr_err[dev] != cudaSuccess)
+        return fail(PDL_ELAUNCH, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err[dev]));
+    int grid = std::min(max_ctas[dev], (work_ctas + CL - 1) / CL * CL);
     if (KIND == pdl::KIND_STEM || RESW) grid = std::max(p.n_tiles, grid / p.n_tiles * p.n_tiles);
     lc.gridDim = dim3(grid);
     pdl::TileParams pt = p;
@@ -284,6 +335,7 @@ struct SplitPlan {
 };
 
 SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int seg_kb, int req) {
+    const int sm_count = sms();
     SplitPlan sp;
     sp.kb_per = num_kb;
     const int tiles = (m_tiles + cl - 1) / cl * cl * n_tiles;
@@ -340,6 +392,7 @@ int bind_split(pdl::TileParams &p, const SplitPlan &sp, void *ws, size_t ws_byte
 
 // GEMM tile choice (shared by the launch and the workspace query).
 void gemm_cfg(int M, int N, const pdl_tile_cfg *cfg_in, int *bn, int *cl, int *raster) {
+    const int sm_count = sms();
     // cluster 1 (no B multicast): equal at 4096^3, 3-10% faster below (r1j A/B)
     // 64-column tiles when 128-column tiles would not fill one wave: small GEMMs are
     // latency-bound chains per tile, and twice the CTAs halve the chain (graph-replayed
@@ -359,7 +412,7 @@ size_t gemm_split_bytes(int M, int N, int K, unsigned flags, const pdl_tile_cfg 
     if (M <= 0 || N <= 0 || K <= 0 || (flags & PDL_MODE_MASK) == PDL_MODE_FP32) return 0;
     int bn, cl, raster;
     gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
-    if (flags & PDL_RELU6) cl = 1;  // extended-epilogue instances are cluster 1
+    if (flags & (PDL_RELU6 | PDL_SCALE)) cl = 1;  // extended-epilogue instances are cluster 1
     if (cl != 1 && cl != 2 && cl != 4) return 0;
     return plan_split((M + 127) / 128, (N + bn - 1) / bn, cl, bn, (K + 31) / 32, kSegElems / 32,
                       cfg_in ? cfg_in->split_k : 0).bytes;
@@ -420,7 +473,7 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool 
             // only when it removes whole waves of the persistent grid: within one wave the
             // per-tile latency is what counts, and a tile spanning images issues 2-3 boxes
             // per k-block (measured 2-6% slower at 32-64 images when the wave count is unchanged)
-            const long long wave = sm_count;
+            const long long wave = sms();
             const long long w_box = ((long long)g.m_tiles * n_tiles + wave - 1) / wave;
             const long long w_seg = (mt * n_tiles + wave - 1) / wave;
             if ((w_seg < w_box || (force_seg && mt < g.m_tiles)) && mt < (1ll << 30)) {
@@ -636,6 +689,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         if ((rc = get_encode())) return rc;
         return conv_fwd_stem(x, wp, bias, y, N, C, K, H, W, R, S, stride, pad, flags, cfg_in, st);
     }
+    if (cfg_in && (cfg_in->raster & ~kRasterBits))
+        return fail(PDL_EUNSUPPORTED, "conv: unsupported raster bits 0x%x", cfg_in->raster & ~kRasterBits);
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
     conv_default_cfg(C, K, R, S, &cfg, flags, !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1)));
@@ -709,7 +764,6 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                       (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
-    const bool blo_onchip = halo && split && cfg_in && (cfg_in->raster & PDL_RASTER_BLO_ONCHIP);
     cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
     if (halo) {
         abox[1] = (cuuint32_t)halo_w;
@@ -721,9 +775,14 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         const cuuint64_t cs = stride == 1 ? 64 : 128, rs = stride == 1 ? (cuuint64_t)W * 64 : (cuuint64_t)W * 128;
         const cuuint64_t dims[5] = {16, (cuuint64_t)Wv, (cuuint64_t)Hv, (cuuint64_t)CT, (cuuint64_t)N};
         const cuuint64_t str[4] = {cs, rs, (cuuint64_t)H * W * 64, (cuuint64_t)CT * H * W * 64};
+        // stride 2 reads every other 64-byte pixel: no 256-byte L2 promotion (it would
+        // fetch the skipped odd pixels too)
+        const CUtensorMapL2promotion l2 = stride == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                      : CU_TENSOR_MAP_L2_PROMOTION_NONE;
         for (int h = 1; h <= std::min(g.seg_tile, g.P); ++h) {
             const cuuint32_t box[5] = {16, (cuuint32_t)g.Q, (cuuint32_t)h, 1, (cuuint32_t)g.seg_imgs};
-            if ((rc = encode(&maps.a[h - 1], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B, "conv x rows")))
+            if ((rc = encode(&maps.a[h - 1], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B, "conv x rows",
+                             l2)))
                 return rc;
             if ((rc = encode_y(&maps.y[h - 1], y, N, KT, g.P, g.Q, g.Q, h, g.seg_imgs))) return rc;
         }
@@ -734,6 +793,13 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         if ((rc = encode(&maps.a[0], x, 5, dims, str, abox, CU_TENSOR_MAP_SWIZZLE_64B, "conv x")))
             return rc;
     } else {
+        // 1-wide filters never read the odd input columns, so a parity map's 64-byte
+        // pixels sit 128 bytes apart and nothing else reads the gaps: 256-byte L2
+        // promotion would fetch every skipped pixel as well (ncu: 1.6x the algorithmic
+        // DRAM bytes on ResNet layers 6/11/16).  Wider filters read the odd columns
+        // through the other parity maps, so the promoted lines are used.
+        const CUtensorMapL2promotion l2 = S == 1 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
         for (int ph = 0; ph < 2; ++ph)
             for (int pw = 0; pw < 2; ++pw) {
                 const cuuint64_t dims[5] = {16, (cuuint64_t)((W - pw + 1) / 2),
@@ -743,7 +809,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                                            (cuuint64_t)CT * H * W * 64};
                 const float *base = x + ((size_t)ph * W + pw) * 16;
                 if ((rc = encode(&maps.a[ph * 2 + pw], base, 5, dims, str, abox,
-                                 CU_TENSOR_MAP_SWIZZLE_64B, "conv x parity")))
+                                 CU_TENSOR_MAP_SWIZZLE_64B, "conv x parity", l2)))
                     return rc;
             }
     }
@@ -761,7 +827,6 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         const bool whole = cl == 1 || pair;
         cuuint32_t bbox[5] = {(cuuint32_t)G, (cuuint32_t)(pair ? cfg.bn / 2 : cfg.bn / cl), 1,
                               (cuuint32_t)(whole ? NB : 1), (cuuint32_t)(whole ? planes : 1)};
-        if (blo_onchip) bbox[4] = 1;  // hi plane only
         if (resident) {
             bbox[1] = (cuuint32_t)cfg.bn;
             bbox[3] = (cuuint32_t)(CT * 16 / G);
@@ -793,8 +858,6 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.BNI = g.BNI;
     p.tiles_w = g.tiles_w;
     p.tiles_h = g.tiles_h;
-    // coalesced LSU epilogue (box tiles only): forced by cfg raster bit 3
-    p.epi_lsu = (!g.seg_mode && cfg_in && (cfg_in->raster & PDL_RASTER_LSU_EPI)) ? 1 : 0;
     p.seg_mode = g.seg_mode;
     p.seg_tile = g.seg_tile;
     p.seg_bytes = g.Q * g.seg_imgs * 64;
@@ -804,7 +867,6 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.n_tiles = n_tiles;
     if ((rc = bind_split(p, spl, ws, ws_bytes, cl))) return rc;
     if (halo) {
-        p.blo_onchip = blo_onchip ? 1 : 0;
         p.box_w = halo_w;
         p.box_h = halo_h;
         return split ? dispatch_halo<true>(cfg.bn, cg, maps, p, st) : dispatch_halo<false>(cfg.bn, cg, maps, p, st);
@@ -822,25 +884,29 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
 }
 
 // ---------------------------------------------------------------- host-buffer pipeline
-// Per-thread, per-device copy streams and slot events of pdl_conv2d_fwd_host.
+// Copy streams and slot events of pdl_conv2d_fwd_host, one set per (device,
+// workspace), in a process-wide table: the relaxed (PDL_HOST_X_READY) ordering
+// depends on the previous call that used the same workspace, whichever thread made
+// it.  The table mutex is held while a call enqueues its work, so calls sharing a
+// workspace from several threads see each other's events in a consistent order.
 constexpr int kHostSlots = 3;     // device staging slots (x and y) in flight
-constexpr int kMaxDevices = 16;
 struct HostPipe {
     bool ready = false;
     cudaStream_t h2d = nullptr, d2h = nullptr, cs = nullptr;  // copies in / out, convolutions
     cudaEvent_t entry = nullptr, x_in[kHostSlots], done[kHostSlots], y_done[2];
     cudaEvent_t x_free = nullptr;     // last conv of the previous call (x area no longer read)
-    const void *last_ws = nullptr;    // workspace of the previous call
+    bool used = false;                // a previous call completed its enqueue on this workspace
     size_t last_ws_bytes = 0;
     int parity = 0;                   // y area half of the next call
 };
-thread_local HostPipe g_pipe[kMaxDevices];
+std::mutex g_pipe_mu;
+std::map<std::pair<int, const void *>, HostPipe> g_pipes;
 
-int host_pipe(HostPipe **out) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
-        return fail(PDL_EDEVICE, "conv host: no current device");
-    HostPipe &hp = g_pipe[dev];
+// caller holds g_pipe_mu
+int host_pipe(const void *ws, HostPipe **out) {
+    const int dev = cur_dev();
+    if (dev < 0) return fail(PDL_EDEVICE, "conv host: no current device");
+    HostPipe &hp = g_pipes[{dev, ws}];
     if (!hp.ready) {
         const unsigned ef = cudaEventDisableTiming;
         bool ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
@@ -901,6 +967,7 @@ int pdl_conv2d_prepack_weights(const float *w, void *packed, int C, int K, int R
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags, "prepack"))) return rc;
     if (C <= 0 || K % 16 || K <= 0 || R <= 0 || S <= 0) return fail(PDL_EINVAL, "prepack: bad shape");
     if (!aligned16(w) || !aligned16(packed)) return fail(PDL_EALIGN, "prepack: unaligned pointer");
     const int split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
@@ -927,6 +994,7 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags, "conv"))) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
     if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
         return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
@@ -955,6 +1023,7 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags, "conv"))) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
     if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
         return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
@@ -986,6 +1055,7 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags | PDL_HOST_X_READY, "conv host"))) return rc;
     if (!x_host || !y_host) return fail(PDL_EINVAL, "conv host: null host buffer");
     if (chunk < 0) return fail(PDL_EINVAL, "conv host: negative chunk");
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
@@ -1001,8 +1071,9 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     const size_t need = pdl_conv2d_host_workspace_bytes(N, C, K, H, W, R, S, stride, pad, chunk);
     if (!workspace || ws_bytes < need)
         return fail(PDL_EWORKSPACE, "conv host: workspace of %zu bytes required", need);
+    std::lock_guard<std::mutex> lock(g_pipe_mu);
     HostPipe *hp;
-    if ((rc = host_pipe(&hp))) return rc;
+    if ((rc = host_pipe(workspace, &hp))) return rc;
     const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
     const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
     const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
@@ -1017,24 +1088,37 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     //   cs : [x_in] conv -> done
     //   d2h: [done] copy y;  after the last chunk -> y_done[q]
     // Default: everything is ordered after prior work on `stream` (entry event).  With
-    // PDL_HOST_X_READY (x_host, packed_w and bias are final at call time) and the
-    // workspace of the previous call, the copies in only wait for that call's last
-    // convolution to release the x area and the convolutions only for their own y area
-    // (the previous call used the other one), so the previous call's copies out overlap
-    // this call's copies in AND convolutions: both PCIe directions stay busy across layers.
-    // `stream` waits for this call's copies out before any later work.
+    // PDL_HOST_X_READY (x_host, packed_w and bias are final at call time, and y_host is
+    // not read by work still pending on `stream`) and a previous call on this workspace,
+    // the copies in only wait for that call's last convolution to release the x area and
+    // the convolutions only for their own y area (the previous call used the other one),
+    // so the previous call's copies out overlap this call's copies in AND convolutions:
+    // both PCIe directions stay busy across layers.  `stream` waits for this call's
+    // copies out before any later work.
     if (cudaEventRecord(hp->entry, st) != cudaSuccess)
         return fail(PDL_ELAUNCH, "conv host: entry event");
-    const bool relaxed = (flags & PDL_HOST_X_READY) && hp->last_ws == workspace && hp->last_ws_bytes == ws_bytes;
+    const bool relaxed = (flags & PDL_HOST_X_READY) && hp->used && hp->last_ws_bytes == ws_bytes;
     if (!relaxed) hp->parity = 0;
     const int q = hp->parity;
     uint8_t *ws_y = ws + (size_t)(1 + q) * third;
+    // A failure after work was enqueued: join what was enqueued into `stream` (later work
+    // on it, and a later call on this workspace, stay ordered after it) and forget the
+    // relaxed-ordering state.
+    auto abort_call = [&](int code) {
+        cudaEventRecord(hp->x_free, hp->cs);
+        cudaEventRecord(hp->y_done[q], hp->d2h);
+        cudaStreamWaitEvent(st, hp->x_free, 0);
+        cudaStreamWaitEvent(st, hp->y_done[q], 0);
+        cudaEventRecord(hp->y_done[q ^ 1], hp->d2h);
+        hp->used = false;
+        return code;
+    };
     if (cudaStreamWaitEvent(hp->h2d, relaxed ? hp->x_free : hp->entry, 0) != cudaSuccess ||
         (!relaxed && cudaStreamWaitEvent(hp->cs, hp->entry, 0) != cudaSuccess))
-        return fail(PDL_ELAUNCH, "conv host: entry wait");
+        return abort_call(fail(PDL_ELAUNCH, "conv host: entry wait"));
     // this y area's previous user (two calls back) must have copied all of it out
     if (cudaStreamWaitEvent(hp->cs, hp->y_done[q], 0) != cudaSuccess)
-        return fail(PDL_ELAUNCH, "conv host: y area wait");
+        return abort_call(fail(PDL_ELAUNCH, "conv host: y area wait"));
     const int nchunks = (N + c - 1) / c;
     int launches = 0;
     for (int i = 0; i < nchunks; ++i) {
@@ -1043,32 +1127,33 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
         float *xd = reinterpret_cast<float *>(ws + b * xs);
         float *yd = reinterpret_cast<float *>(ws_y + n0 * y_img);
         if (i >= kHostSlots && cudaStreamWaitEvent(hp->h2d, hp->done[b], 0) != cudaSuccess)
-            return fail(PDL_ELAUNCH, "conv host: wait");
+            return abort_call(fail(PDL_ELAUNCH, "conv host: wait"));
         if (cudaMemcpyAsync(xd, reinterpret_cast<const uint8_t *>(x_host) + n0 * x_img, n * x_img,
                             cudaMemcpyHostToDevice, hp->h2d) != cudaSuccess ||
             cudaEventRecord(hp->x_in[b], hp->h2d) != cudaSuccess)
-            return fail(PDL_ELAUNCH, "conv host: H2D copy: %s", cudaGetErrorString(cudaGetLastError()));
+            return abort_call(fail(PDL_ELAUNCH, "conv host: H2D copy: %s", cudaGetErrorString(cudaGetLastError())));
         if (cudaStreamWaitEvent(hp->cs, hp->x_in[b], 0) != cudaSuccess)
-            return fail(PDL_ELAUNCH, "conv host: wait");
+            return abort_call(fail(PDL_ELAUNCH, "conv host: wait"));
         if ((rc = conv_fwd_tc(xd, reinterpret_cast<const float *>(packed_w), bias, yd, n, C, K, H, W,
                               R, S, stride, pad, cflags, cfg, hp->cs)))
-            return rc;
+            return abort_call(rc);
         launches += g_launches;
         if (cudaEventRecord(hp->done[b], hp->cs) != cudaSuccess ||
             cudaStreamWaitEvent(hp->d2h, hp->done[b], 0) != cudaSuccess ||
             cudaMemcpyAsync(reinterpret_cast<uint8_t *>(y_host) + n0 * y_img, yd, n * y_img,
                             cudaMemcpyDeviceToHost, hp->d2h) != cudaSuccess)
-            return fail(PDL_ELAUNCH, "conv host: D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+            return abort_call(fail(PDL_ELAUNCH, "conv host: D2H copy: %s", cudaGetErrorString(cudaGetLastError())));
     }
     // the x area is free once the last convolution has run (next call's copies in)
-    if (cudaEventRecord(hp->x_free, hp->cs) != cudaSuccess) return fail(PDL_ELAUNCH, "conv host: x_free");
-    hp->last_ws = workspace;
-    hp->last_ws_bytes = ws_bytes;
-    hp->parity = q ^ 1;
+    if (cudaEventRecord(hp->x_free, hp->cs) != cudaSuccess)
+        return abort_call(fail(PDL_ELAUNCH, "conv host: x_free"));
     // later work on `stream` sees every y copy (and so every convolution) done
     if (cudaEventRecord(hp->y_done[q], hp->d2h) != cudaSuccess ||
         cudaStreamWaitEvent(st, hp->y_done[q], 0) != cudaSuccess)
-        return fail(PDL_ELAUNCH, "conv host: exit wait");
+        return abort_call(fail(PDL_ELAUNCH, "conv host: exit wait"));
+    hp->used = true;
+    hp->last_ws_bytes = ws_bytes;
+    hp->parity = q ^ 1;
     g_launches = launches;
     return PDL_OK;
 }
@@ -1080,6 +1165,7 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags, "conv"))) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
     if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
         return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
@@ -1106,32 +1192,40 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
     return rc;
 }
 
-int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda, int ldb,
-                 int ldc, float alpha, float beta, unsigned flags, const pdl_tile_cfg *cfg_in,
-                 void *workspace, size_t ws_bytes, void *stream) {
+int pdl_gemm_f32_epilogue(const float *A, const float *B, float *C, const float *bias, int M, int N, int K,
+                          int lda, int ldb, int ldc, float alpha, float beta, unsigned flags,
+                          const pdl_tile_cfg *cfg_in, void *workspace, size_t ws_bytes, void *stream) {
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kGemmFlags, "gemm"))) return rc;
     if (M < 0 || N < 0 || K < 0) return fail(PDL_EINVAL, "gemm: negative dimension");
     if (lda < std::max(K, 1) || ldb < std::max(N, 1) || ldc < std::max(N, 1))
         return fail(PDL_EINVAL, "gemm: leading dimension too small");
+    if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
+        return fail(PDL_EALIGN, "gemm: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias[N] (shift[N] | scale[N])");
     if (M == 0 || N == 0) return PDL_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned mode = flags & PDL_MODE_MASK;
+    const unsigned eflags = flags & (kEpiFlags | kDiag);
+    const float *ebias = (flags & (PDL_BIAS | PDL_SCALE)) ? bias : nullptr;
+    // TMA describes the operands only with 16-byte aligned bases and row strides
     const bool tma_ok = K > 0 && aligned16(A) && aligned16(B) && aligned16(C) && lda % 4 == 0 &&
-                        ldb % 4 == 0 && ldc % 4 == 0 && N % 4 == 0 &&
-                        (!(flags & PDL_BIAS) || (cfg_in == nullptr || true));
+                        ldb % 4 == 0 && ldc % 4 == 0 && N % 4 == 0;
+    if (mode != PDL_MODE_FP32 && !tma_ok && (flags & PDL_NO_SIMT))
+        return fail(PDL_EUNSUPPORTED, "gemm: tensor-core path needs K > 0, 16-byte aligned A/B/C and "
+                    "N, lda, ldb, ldc multiples of 4 (PDL_NO_SIMT forbids the CUDA-core path)");
     if (mode == PDL_MODE_FP32 || !tma_ok) {
         dim3 grid((N + 63) / 64, (M + 63) / 64);
-        pdl::simt_gemm_kernel<<<grid, 256, 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc, alpha, beta,
-                                                    nullptr, flags & ~(unsigned)PDL_BIAS);
+        pdl::simt_gemm_kernel<<<grid, 256, 0, st>>>(A, B, C, M, N, K, lda, ldb, ldc, alpha, beta, ebias,
+                                                    eflags);
         ++g_launches;
         return check_launch("simt_gemm_kernel");
     }
     if ((rc = get_encode())) return rc;
     int bn, cl, raster;
     gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
-    const bool epix = flags & PDL_RELU6;  // extended-epilogue instances are cluster 1
+    const bool epix = flags & (PDL_RELU6 | PDL_SCALE);  // extended-epilogue instances are cluster 1
     if (epix) cl = 1;
     if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "gemm: cluster_m must be 1, 2 or 4");
     pdl::TmaMaps maps;
@@ -1152,8 +1246,8 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     p.num_kb = (K + 31) / 32;
     p.seg_kb = kSegElems / 32;
     p.n_out = N;
-    p.flags = flags & ~(unsigned)PDL_BIAS;
-    p.bias = nullptr;
+    p.flags = eflags;
+    p.bias = ebias;
     p.out = C;
     p.M = M;
     p.ldc = ldc;
@@ -1175,11 +1269,23 @@ int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, 
     return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, cl, maps, p, st);
 }
 
+int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda, int ldb,
+                 int ldc, float alpha, float beta, unsigned flags, const pdl_tile_cfg *cfg_in,
+                 void *workspace, size_t ws_bytes, void *stream) {
+    if (flags & (PDL_BIAS | PDL_SCALE)) {
+        g_launches = 0;
+        return fail(PDL_EINVAL, "gemm: PDL_BIAS / PDL_SCALE take a bias vector: use pdl_gemm_f32_epilogue");
+    }
+    return pdl_gemm_f32_epilogue(A, B, C, nullptr, M, N, K, lda, ldb, ldc, alpha, beta, flags, cfg_in,
+                                 workspace, ws_bytes, stream);
+}
+
 int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int Q, unsigned flags,
                           void *stream) {
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags, "bias_relu"))) return rc;
     if (K % 16 || N < 0 || P < 0 || Q < 0) return fail(PDL_EINVAL, "bias_relu: bad shape");
     if (!aligned16(y) || ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias))))
         return fail(PDL_EALIGN, "bias_relu: unaligned pointer");
@@ -1190,6 +1296,25 @@ int pdl_bias_relu_nchw16c(float *y, const float *bias, int N, int K, int P, int 
         reinterpret_cast<float4 *>(y), bias, n4, P * Q, K / 16, flags);
     ++g_launches;
     return check_launch("bias_relu_kernel");
+}
+
+int pdl_accumulate_epilogue_nchw16c(float *y, const float *y0, const float *bias, int N, int K, int P,
+                                    int Q, unsigned flags, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = device_check())) return rc;
+    if ((rc = check_flags(flags, kConvFlags, "accumulate"))) return rc;
+    if (K % 16 || N < 0 || P < 0 || Q < 0) return fail(PDL_EINVAL, "accumulate: bad shape");
+    if (!y0) return fail(PDL_EINVAL, "accumulate: null addend");
+    if (!aligned16(y) || !aligned16(y0) || ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias))))
+        return fail(PDL_EALIGN, "accumulate: unaligned pointer");
+    const long long n4 = (long long)N * K * P * Q / 4;
+    if (n4 == 0) return PDL_OK;
+    const int blocks = (int)std::min<long long>((n4 + 255) / 256, 148LL * 8);
+    pdl::accumulate_epilogue_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<float4 *>(y), reinterpret_cast<const float4 *>(y0), bias, n4, P * Q, K / 16, flags);
+    ++g_launches;
+    return check_launch("accumulate_epilogue_kernel");
 }
 
 static int layout_check(const void *a, const void *b, long long n) {

@@ -37,8 +37,10 @@ namespace pdl {
 
 enum { KIND_GEMM = 0, KIND_CONV = 1, KIND_STEM = 2 };
 
-// Diagnostic switches (flags bits >= 8, never set by the public API wrappers):
-// results are WRONG when set; used only to attribute time between pipeline roles.
+// Diagnostic switches (flags bits >= 8): results are WRONG when set; used only to
+// attribute time between pipeline roles (scripts/probe_*roles*.py).  Compiled in only
+// with -DPDL_DIAG (PDL_DIAG=1 python -m paper_2006_02230_b200.build): the product
+// library has no such branches and rejects the bits.
 enum : unsigned {
     DBG_NO_A_TMA = 1u << 8,     // producer skips the A loads
     DBG_NO_STAGE_ST = 1u << 9,  // staging warps skip the tcgen05.st into TMEM
@@ -46,6 +48,12 @@ enum : unsigned {
     DBG_NO_MMA = 1u << 11,        // MMA warp commits without issuing the MMAs
     DBG_NO_GATHER = 1u << 12      // stem staging skips the halo reads (stores zeros)
 };
+constexpr unsigned kDiagBits = 0x1f00u;
+#ifdef PDL_DIAG
+#define PDL_DBG(p, bit) (((p).flags & (bit)) != 0)
+#else
+#define PDL_DBG(p, bit) false
+#endif
 
 // Geometry / epilogue parameters (by value, param space).
 struct TileParams {
@@ -72,13 +80,6 @@ struct TileParams {
     // offsets (TMA swizzles by absolute smem address, so the stack is the canonical SW64
     // tile; the epilogue stores the same boxes).  seg_mode 0: box tiles.
     int seg_mode, seg_tile, seg_bytes, seg_imgs;
-    // conv epilogue: 0 = TMA box stores; 1 = warp-local smem transpose + coalesced
-    // st.global.v4 (each instruction writes 8 whole 64-byte pixels; no TMA engine, no
-    // bulk-group waits, no 128-thread barriers).  Box tiles only.
-    int epi_lsu;
-    // halo 3xTF32 convs: load only the weights' hi plane; the staging warps form
-    // lo = w - tf32(w) in the stage (halves the weights' TMA fill)
-    int blo_onchip;
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
@@ -144,9 +145,6 @@ constexpr int kStemHaloBytes = 16384;
 // output-box ring depth for the output-heavy resident-weight 1x1 convs: their epilogue
 // is the bottleneck -- a 16-channel box store takes ~1000 cycles to
 // release its smem (traces: ResNet layers 4/8 spend 4100-4300 cycles per tile storing)
-#ifndef PDL_BATCH_ALL  // experiments: batched box stores wherever a buffer per box exists
-#define PDL_BATCH_ALL 0
-#endif
 #ifndef PDL_STEM_WIDE_EPI
 #define PDL_STEM_WIDE_EPI 0
 #endif
@@ -232,10 +230,8 @@ struct Smem {
     // one drains (one buffer serialised the epilogue on each TMA store's smem read)
     // (only where smem keeps >= 4 stages: with 64 KB weight planes a 4-deep ring leaves
     // 2 stages and layer 5 ran 28% slower; the stem measured no change)
-    static constexpr bool WIDE_FITS =
-        (232448 - 2048 - W_BYTES - HALO_BYTES - 2 * PDL_EPI_BUFS_WIDE * 8192) / STAGE >= 3;
-    static constexpr int EPI_BUFS = ((RESW > 0 && RESW <= 32768) || (KIND == KIND_STEM && PDL_STEM_WIDE_EPI) ||
-                                     (PDL_BATCH_ALL && KIND == KIND_CONV && !RESW && WIDE_FITS))
+    // (batched 4-deep rings on every BN=128 layer cost those layers a stage: 3-15% slower)
+    static constexpr int EPI_BUFS = ((RESW > 0 && RESW <= 32768) || (KIND == KIND_STEM && PDL_STEM_WIDE_EPI))
                                         ? PDL_EPI_BUFS_WIDE : PDL_EPI_BUFS;
     static constexpr int EPI_BYTES = KIND == KIND_GEMM ? 0 : 2 * EPI_BUFS * 8192;
     // 227 KB opt-in dynamic smem per CTA, minus 2 KB for barriers + base alignment
@@ -573,8 +569,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t tx;
             if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
             else if (KIND == KIND_CONV)
-                tx = (uint32_t)(((p.flags & DBG_NO_A_TMA) || HALO ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
-                                (RESW ? 0 : G::B_BYTES * (p.blo_onchip ? 1 : L::LOAD_PLANES)));
+                tx = (uint32_t)((PDL_DBG(p, DBG_NO_A_TMA) || HALO ? 0 : CG * 64 * p.BW * p.BH * p.BNI) +
+                                (RESW ? 0 : G::B_BYTES * L::LOAD_PLANES));
             else tx = (uint32_t)(16 * p.box_w * p.box_h * (p.halo_odd ? 2 : 1));
             // HALO: one box of (box_w x box_h x BNI) pixels per 16-channel sub-tile
             const uint32_t htx = (uint32_t)(CG * 64 * p.box_w * p.box_h * p.BNI);
@@ -667,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             dh = (dh - ph2) >> 1;
                             dw = (dw - pw2) >> 1;
                         }
-                        if ((p.flags & DBG_NO_A_TMA) || HALO) {
+                        if (PDL_DBG(p, DBG_NO_A_TMA) || HALO) {
                         } else if (p.seg_mode) {
                             // bands p0.. of image group i0, then the next group(s) from row 0
                             int grp = tc.i0, r = tc.p0, left = p.seg_tile, off = 0;
@@ -771,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             bhi = smem_desc(w, PL * BN * 16, 128, 0);
                             blo = smem_desc(w + BN * 16, PL * BN * 16, 128, 0);
                         }
-                        if (p.flags & DBG_NO_MMA) {
+                        if (PDL_DBG(p, DBG_NO_MMA)) {
                         } else if constexpr (PAIR) {
                             mma_ts_block2<G::NK, SPLIT3, G::KS, G::boff(0), G::boff(1), G::boff(2),
                                           G::boff(3), G::boff(4), G::boff(5), G::boff(6), G::boff(7)>(
@@ -899,12 +895,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int c = 0; c < 5; ++c) {
                             float x[16], lo[16];
-                            const bool lv = live && !(p.flags & DBG_NO_GATHER);
+                            const bool lv = live && !PDL_DBG(p, DBG_NO_GATHER);
                             if (kb == 0) stem_gather_kb<0>(c, sa, row_step, col, lv, x);
                             else stem_gather_kb<1>(c, sa, row_step, col, lv, x);
 #pragma unroll
                             for (int i = 0; i < 16; ++i) lo[i] = tf32_lo(x[i]);
-                            if (!(p.flags & DBG_NO_STAGE_ST)) {
+                            if (!PDL_DBG(p, DBG_NO_STAGE_ST)) {
                                 tmem_st16(t_hi + c * 16, x);
                                 if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
                             }
@@ -931,7 +927,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (tr) trace_ev(p, TR_S_TFREE, kglob);
                     tc_fence_after();
                     const uint32_t t_hi = tmem_base + lane_off + L::A_SLOT0 + t * L::SLOT_COLS;
-                    if (!(p.flags & DBG_NO_STAGE_ST)) {
+                    if (!PDL_DBG(p, DBG_NO_STAGE_ST)) {
                         tmem_st32(t_hi, x);
                         if (SPLIT3) tmem_st32(t_hi + G::KS, lo);
                     }
@@ -972,13 +968,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // the stage's B (and A, without HALO) landed: tready below is what the MMA
                     // warp waits on, so it must imply B is in shared memory
                     mbar_wait(&full[s], ph);
-                    if constexpr (HALO && SPLIT3) {
-                        if (p.blo_onchip) {  // weights' lo plane from the landed hi plane
-                            split_lo_smem(smem0 + s * L::STAGE + L::B_HI, smem0 + s * L::STAGE + L::B_LO,
-                                          G::B_BYTES, tid, 128);
-                            fence_proxy_async_smem();  // generic writes -> tensor core (async proxy)
-                        }
-                    }
                     if constexpr (HALO) {
                         const int rs_n = p.R * p.S;
                         const int rs = kb - (kb / rs_n) * rs_n;
@@ -1039,7 +1028,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&tfree[t], tph ^ 1);
                         if (tr) trace_ev(p, TR_S_TFREE, kglob);
                         tc_fence_after();
-                        if (!(p.flags & DBG_NO_STAGE_ST)) {
+                        if (!PDL_DBG(p, DBG_NO_STAGE_ST)) {
                             // fully unrolled: x[] must stay in registers and the warp-collective
                             // tcgen05.st must not sit in a data-dependent loop
 #pragma unroll
@@ -1116,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     fence_proxy_async_smem();
                     named_bar_sync(2 + half, 128);
                     if (leader) {
-                        if (col0 < p.n_out && !(p.flags & DBG_NO_EPI_STORE)) {
+                        if (col0 < p.n_out && !PDL_DBG(p, DBG_NO_EPI_STORE)) {
                             if (p.seg_mode) {
                                 int grp = tc.i0, r = tc.p0, left = p.seg_tile;
                                 uint32_t off = 0;
@@ -1246,50 +1235,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (KIND == KIND_CONV && p.epi_lsu) {
-                // ---- coalesced LSU store (bias + ReLU fused): the warp writes its 32 pixels'
-                // 16-channel block into a private 2 KB smem scratch (SW64-style XOR, conflict
-                // free), then lane t stores 16 bytes of pixel 8i + t/4: 512 contiguous bytes
-                // per instruction wherever the pixels are consecutive in y
-                const uint32_t wbuf = smem0 + L::EPI_OFF + (uint32_t)e * 2048;
-                const int per_img = p.BW * p.BH;
-                const size_t plane = (size_t)p.P * p.Q * 16;
-                // output pixel offsets (floats, channel block 0) of the 4 pixels this lane stores
-                long long off[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int r = quarter * 32 + 8 * i + (lane >> 2);
-                    const int il = r / per_img, rem = r - il * per_img;
-                    const int hl = rem / p.BW, wl = rem - hl * p.BW;
-                    const int img = tc.i0 + il, pp = tc.p0 + hl, qq = tc.q0 + wl;
-                    const bool ok = r < per_img * p.BNI && il < p.BNI && img < p.nimg && pp < p.P && qq < p.Q;
-                    off[i] = ok ? ((long long)img * p.KT * plane + ((size_t)pp * p.Q + qq) * 16 + (lane & 3) * 4) : -1;
-                }
-#pragma unroll
-                for (int j = 0; j < HALF / 16; ++j) {
-                    const int col0 = tc.n0 + half * HALF + j * 16;
-                    if (col0 >= p.n_out) break;
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        float4 r = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
-                                               sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
-                        r = epilogue4<EPIX>(p.flags, p.bias, p.n_out, col0 + q4 * 4, r);
-                        sts128(wbuf + lane * 64 + ((q4 ^ ((lane >> 1) & 3)) << 4), r);
-                    }
-                    __syncwarp();
-                    float *ycol = p.out + (size_t)(col0 >> 4) * plane;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int px = 8 * i + (lane >> 2), c = lane & 3;
-                        const float4 v = lds128(wbuf + px * 64 + ((c ^ ((px >> 1) & 3)) << 4));
-                        if (off[i] >= 0 && !(p.flags & DBG_NO_EPI_STORE))
-                            *reinterpret_cast<float4 *>(ycol + off[i]) = v;
-                    }
-                    __syncwarp();
-                }
-                if (tr) trace_ev(p, TR_E_STORED, jt);
-                continue;
-            }
             if constexpr (KIND != KIND_GEMM) {
                 // ---- store via TMA (bias + ReLU fused): per 16-channel block, the half's
                 // 128 threads write their pixel's 64 bytes into a SW64 smem image of the
@@ -1299,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool leader = quarter == 0 && lane == 0;
                 // one 16-channel output box of this tile from smem buffer `ebuf`
                 auto store_box = [&](uint32_t ebuf, int col0) {
-                    if (col0 >= p.n_out || (p.flags & DBG_NO_EPI_STORE)) {
+                    if (col0 >= p.n_out || PDL_DBG(p, DBG_NO_EPI_STORE)) {
                     } else if (p.seg_mode) {
                         int grp = tc.i0, r = tc.p0, left = p.seg_tile;
                         uint32_t off = 0;
@@ -1325,7 +1270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sts128(ebuf + row * 64 + ((q4 ^ ((row >> 1) & 3)) << 4), r);
                     }
                 };
-                if constexpr (L::EPI_BUFS >= HALF / 16 && (RESW || KIND == KIND_STEM || PDL_BATCH_ALL)) {
+                if constexpr (L::EPI_BUFS >= HALF / 16 && (RESW || KIND == KIND_STEM)) {
                     // output-heavy tiles with a buffer per box: write every box of the tile,
                     // then store them all (2 barriers per tile instead of 2 per box; stem
                     // -6%, layers 2/4 -5/-11%; compute-bound BN=64 layer 3 keeps the ring)
@@ -1383,7 +1328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ((size_t)(valid ? pp : 0) * p.Q + (valid ? qq : 0)) * 16;
                 cstride = plane;  // next 16-channel block kt
             }
-            if (valid && !(p.flags & DBG_NO_EPI_STORE)) {
+            if (valid && !PDL_DBG(p, DBG_NO_EPI_STORE)) {
 #pragma unroll
                 for (int j = 0; j < HALF / 16; ++j) {
                     const int col0 = tc.n0 + half * HALF + j * 16;
@@ -1513,6 +1458,22 @@ __global__ void bias_relu_kernel(float4 *__restrict__ y, const float *__restrict
          i += (long long)gridDim.x * blockDim.x) {
         const int kt = (int)((i / (4LL * pq)) % KT);
         y[i] = epilogue4<true>(flags, bias, KT * 16, kt * 16 + (int)(i & 3) * 4, y[i]);
+    }
+}
+
+// `+=` of a conv result onto non-zero incoming output contents, then the epilogue:
+// y = act((y + y0) * scale + bias) over nKhw16k (the executor's accumulating nests).
+__global__ void accumulate_epilogue_kernel(float4 *__restrict__ y, const float4 *__restrict__ y0,
+                                           const float *__restrict__ bias, long long n4, int pq, int KT,
+                                           unsigned flags) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int kt = (int)((i / (4LL * pq)) % KT);
+        float4 v = y[i];
+        const float4 a = y0[i];
+        v.x = __fadd_rn(v.x, a.x); v.y = __fadd_rn(v.y, a.y);
+        v.z = __fadd_rn(v.z, a.z); v.w = __fadd_rn(v.w, a.w);
+        y[i] = epilogue4<true>(flags, bias, KT * 16, kt * 16 + (int)(i & 3) * 4, v);
     }
 }
 

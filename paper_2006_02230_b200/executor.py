@@ -445,13 +445,23 @@ def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
         shapes.update(n.shapes(binding))
     dev = torch.device(device) if device is not None else torch.device("cuda")
     arrays: dict = {}
+    nonzero: dict = {}   # host-side: does the incoming array hold anything but zeros?
     for name, shape in shapes.items():
         if name not in inputs:
             raise InterpreterError(f"input array {name!r} missing")
         need = int(np.prod(shape)) if shape else 1
-        if np.asarray(inputs[name]).size < need:
-            raise InterpreterError(f"input array {name!r} too small")
-        arrays[name] = _as_float32_device(torch, inputs[name], shape, dev)
+        host = inputs[name]
+        if isinstance(host, np.ndarray) or not hasattr(host, "is_cuda"):
+            host = np.asarray(host)
+            if host.size < need:
+                raise InterpreterError(f"input array {name!r} too small")
+            nonzero[name] = bool(np.any(host.ravel()[:need] != 0))
+            arrays[name] = _as_float32_device(torch, host, shape, dev)
+        else:                          # a device tensor (keep_on_device chaining)
+            if host.numel() < need:
+                raise InterpreterError(f"input array {name!r} too small")
+            nonzero[name] = True       # unknown without a device sync: accumulate
+            arrays[name] = host.reshape(-1)[:need].to(dev, torch.float32).reshape(shape)
     for plan in plans:
         if isinstance(plan, ConvPlan):
             y0 = arrays[plan.out]
@@ -459,43 +469,37 @@ def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
             w = arrays[plan.filt]
             ep = plan.epilogue
             kw = _epilogue_args(ep, arrays, plan.KT * 16)
-            accumulate = bool(torch.any(y0 != 0))
+            accumulate = nonzero.get(plan.out, True)
             fuse = ep is not None and not accumulate
             y = ops.conv2d_nchw16c(x.contiguous(), w.contiguous(), stride=plan.stride, pad=0,
                                    mode=mode, **(kw if fuse else {}))
-            y = y[:, :, :plan.P, :plan.Q, :]
-            if accumulate:           # `+=` onto non-zero incoming contents
-                y = (y + y0).contiguous()
-                if ep is not None:   # the epilogue after the accumulation, on the GPU
-                    ops.bias_relu_(y, **kw)
-            arrays[plan.out] = y.contiguous()
+            y = y[:, :, :plan.P, :plan.Q, :].contiguous()
+            if accumulate:           # `+=` onto non-zero incoming contents (+ the epilogue)
+                ops.accumulate_(y, y0.contiguous(), **kw)
+            arrays[plan.out] = y
+            nonzero[plan.out] = True
         elif isinstance(plan, GemmPlan):
-            c0 = arrays[plan.C]
             a = arrays[plan.A][:plan.M, :plan.K].contiguous()
             b = arrays[plan.B][:plan.K, :plan.N].contiguous()
             ep = plan.epilogue
-            beta = 1.0 if bool(torch.any(c0 != 0)) else 0.0
-            c = c0.clone() if beta else torch.empty_like(c0)
-            # pdl_gemm_f32 fuses ReLU / ReLU6; a GEMM bias or scale has no C-ABI slot
-            fuse_act = ep is not None and ep.bias is None and ep.scale is None
-            ops.gemm(a, b, c, beta=beta, relu=fuse_act and ep.relu, relu6=fuse_act and ep.relu6,
-                     mode=mode)
-            if ep is not None and not fuse_act:
-                if ep.scale is not None:
-                    c = c * arrays[ep.scale].reshape(1, -1)[:, :plan.N]
-                if ep.bias is not None:
-                    c = c + arrays[ep.bias].reshape(1, -1)[:, :plan.N]
-                if ep.relu or ep.relu6:
-                    c = torch.where(0.0 > c, torch.zeros_like(c), c)
-                if ep.relu6:
-                    c = torch.where(6.0 < c, torch.full_like(c, 6.0), c)
+            # `+=` onto non-zero incoming C: beta = 1 inside the kernel, C updated in place
+            beta = 1.0 if nonzero.get(plan.C, True) else 0.0
+            c = arrays[plan.C].contiguous()
+            ekw = {}
+            if ep is not None:
+                vec = lambda nm: None if nm is None else arrays[nm].reshape(-1)[:plan.N].contiguous()  # noqa: E731
+                ekw = {"bias": vec(ep.bias), "scale": vec(ep.scale), "relu": ep.relu and not ep.relu6,
+                       "relu6": ep.relu6}
+            ops.gemm(a, b, c, beta=beta, mode=mode, **ekw)
             arrays[plan.C] = c
+            nonzero[plan.C] = True
         else:  # stand-alone element-wise nest (no preceding heavy nest to fuse into)
             y = arrays[plan.target]
             if y.dim() == 5 and y.shape[-1] == 16 and plan.channel_axes_ok((1, 4)):
                 y = y.contiguous()
                 ops.bias_relu_(y, **_epilogue_args(plan, arrays, y.shape[1] * 16))
                 arrays[plan.target] = y
+                nonzero[plan.target] = True
                 continue
             raise InterpreterError(f"element-wise nest {plan.nest!r} is only supported on nChw16c "
                                    "conv outputs (channel-indexed bias / scale) or fused after a "
@@ -506,14 +510,22 @@ def execute(nests, binding: Mapping[str, int], inputs: Mapping[str, np.ndarray],
 
 
 def interpret(nest, binding: Mapping[str, int], seed: int = 0,
-              inputs: Mapping[str, np.ndarray] | None = None, collect_trace: bool = False,
+              inputs: Mapping[str, np.ndarray] | None = None, collect_trace: bool = True,
               mode: str = "3xtf32"):
-    """Drop-in for `looprank.simcache.interpret` on the hot path: returns
-    (arrays, None).  Access traces belong to the CPU cache simulator, which is
-    out of scope on B200 (collect_trace=True raises)."""
-    if collect_trace:
-        raise InterpreterError("the B200 executor does not record element access traces")
+    """Drop-in for `looprank.simcache.interpret` (simcache.py:89-204), same
+    signature and defaults: returns (arrays, trace).  The arrays are computed on
+    the B200.  The trace (collect_trace=True, the reference's default) is a
+    `trace.LazyTrace`: the reference's TraceRecord sequence, generated on the host
+    from the nest structure when first used (it does not depend on the values);
+    for a Program, a tuple with one LazyTrace per nest.  collect_trace=False
+    returns None, as the reference returns an empty Trace's records."""
+    from .trace import LazyTrace
     first = nest.nests[0] if isinstance(nest, Program) else nest
     if inputs is None:
         inputs = make_inputs(first, binding, seed)
-    return execute(nest, binding, inputs, mode=mode), None
+    arrays = execute(nest, binding, inputs, mode=mode)
+    if not collect_trace:
+        return arrays, None
+    if isinstance(nest, Program):
+        return arrays, tuple(LazyTrace(n, binding) for n in nest.nests)
+    return arrays, LazyTrace(nest, binding)

@@ -9,14 +9,21 @@ Layouts (the reference nest's array declarations):
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import warnings
 from dataclasses import dataclass
 
 import torch
 
 from . import _lib
-from ._lib import (PDL_BIAS, PDL_HOST_X_READY, PDL_OP_GEMM, PDL_RELU, PDL_RELU6, PDL_SCALE, MODES,
-                   TileCfg, check, lib)
+from ._lib import (PDL_BIAS, PDL_HOST_X_READY, PDL_MODE_FP32, PDL_NO_SIMT, PDL_OP_GEMM, PDL_RELU,
+                   PDL_RELU6, PDL_SCALE, MODES, TileCfg, check, lib)
+
+
+class SimtPathWarning(UserWarning):
+    """A tensor-core-mode GEMM ran on the CUDA cores (exact fp32) because TMA
+    cannot describe its operands (N or K not a multiple of 4, unaligned views)."""
 
 
 def _mode(mode: str) -> int:
@@ -29,6 +36,14 @@ def _mode(mode: str) -> int:
 def _stream(stream) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+def _on(stream):
+    """Allocate (and zero) temporaries on the stream the library call runs on: the
+    caching allocator then reuses their blocks only in that stream's order, so a
+    temporary freed when the Python call returns is never handed out while a
+    kernel on `stream` may still read it."""
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
 def _ptr(t):
@@ -62,7 +77,8 @@ def _split_workspace(device, stream_handle: int, nbytes: int):
     """Zero-initialised split-K workspace, one per (device, stream): its tile
     counters reset themselves at the end of every launch, so concurrent streams
     must not share one.  Buffers are only ever added (a CUDA graph captured
-    earlier keeps pointing at the old one), growing 2x at a time."""
+    earlier keeps pointing at the old one), growing 2x at a time.  Called under
+    `_on(stream)`: the zero fill is ordered before the kernels that use it."""
     if nbytes == 0:
         return None
     key = (torch.device(device).index, stream_handle)
@@ -156,6 +172,13 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
     if not (ct * 16 - 16 < C <= ct * 16):
         raise ValueError(f"channel mismatch: x has {ct} blocks of 16, w has C={C}")
     P, Q = conv_out_hw(h, wd, R, S, stride, pad)
+    with _on(stream):
+        return _conv2d_call(x, w, packed, bias, out, n, C, K, h, wd, R, S, P, Q, stride, pad, relu,
+                            relu6, scale, mode, cfg, stream)
+
+
+def _conv2d_call(x, w, packed, bias, out, n, C, K, h, wd, R, S, P, Q, stride, pad, relu, relu6,
+                 scale, mode, cfg, stream):
     y = out if out is not None else torch.empty((n, K // 16, P, Q, 16), dtype=torch.float32,
                                                 device=x.device)
     _need_cuda_f32("out", y)
@@ -233,7 +256,8 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     need = lib().pdl_conv2d_host_workspace_bytes(n, w.C, w.K, h, wd, w.R, w.S, stride, pad, chunk)
     sh = _stream(stream)
     ws = _host_workspace(dev, sh, need)
-    eflags, bias = _epilogue(bias, relu, relu6, scale, w.K)
+    with _on(stream):
+        eflags, bias = _epilogue(bias, relu, relu6, scale, w.K)
     flags = _mode(mode) | eflags
     if x_ready and scale is None:   # (a fused scale builds its [shift | scale] buffer on `stream`)
         flags |= PDL_HOST_X_READY
@@ -245,27 +269,43 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha: float = 1.0,
          beta: float = 0.0, relu: bool = False, mode: str = "3xtf32", cfg=None,
-         stream=None, relu6: bool = False) -> torch.Tensor:
-    """C = act(alpha * A @ B + beta * C) (row-major fp32), act = ReLU / ReLU6 / none."""
+         stream=None, relu6: bool = False, bias: torch.Tensor | None = None,
+         scale: torch.Tensor | None = None, strict: bool = False) -> torch.Tensor:
+    """C = act((alpha * A @ B + beta * C) * scale[n] + bias[n]) (row-major fp32), act =
+    ReLU / ReLU6 / none, scale and bias optional (the fused GEMM epilogue of Alg. 3,
+    PAPER.md:1228-1241).  Shapes the tensor cores cannot take through TMA (N or K not
+    a multiple of 4) run on the CUDA cores in exact fp32 with a SimtPathWarning;
+    strict=True raises instead."""
     for nm, t in (("a", a), ("b", b)):
         _need_cuda_f32(nm, t)
     m, k = a.shape
     k2, n = b.shape
     if k != k2:
         raise ValueError(f"inner dimensions differ: {k} vs {k2}")
-    if c is None:
-        if beta != 0.0:
-            raise ValueError("beta != 0 needs c")
-        c = torch.empty((m, n), dtype=torch.float32, device=a.device)
-    _need_cuda_f32("c", c)
-    flags = _mode(mode) | (PDL_RELU if relu else 0) | (PDL_RELU6 if relu6 else 0)
-    cp = _cfg_ptr(cfg)
-    sh = _stream(stream)
-    dims = (ctypes.c_int * 4)(m, n, k, flags)
-    need = lib().pdl_workspace_bytes(PDL_OP_GEMM, dims, cp)
-    ws = _split_workspace(a.device, sh, need)
-    check(lib().pdl_gemm_f32(_ptr(a), _ptr(b), _ptr(c), m, n, k, k, n, n, float(alpha),
-                             float(beta), flags, cp, _ptr(ws), need, ctypes.c_void_p(sh)))
+    with _on(stream):
+        if c is None:
+            if beta != 0.0:
+                raise ValueError("beta != 0 needs c")
+            c = torch.empty((m, n), dtype=torch.float32, device=a.device)
+        _need_cuda_f32("c", c)
+        eflags, ebuf = _epilogue(bias, relu, relu6, scale, n)
+        flags = _mode(mode) | eflags
+        if (flags & 0x30) != PDL_MODE_FP32 and m and n and not (
+                k > 0 and n % 4 == 0 and k % 4 == 0 and
+                all(t.data_ptr() % 16 == 0 for t in (a, b, c))):
+            if strict:
+                flags |= PDL_NO_SIMT
+            else:
+                warnings.warn(f"gemm {m}x{n}x{k}: operands not TMA-describable, running the exact-fp32 "
+                              "CUDA-core kernel", SimtPathWarning, stacklevel=2)
+        cp = _cfg_ptr(cfg)
+        sh = _stream(stream)
+        dims = (ctypes.c_int * 4)(m, n, k, flags)
+        need = lib().pdl_workspace_bytes(PDL_OP_GEMM, dims, cp)
+        ws = _split_workspace(a.device, sh, need)
+        check(lib().pdl_gemm_f32_epilogue(_ptr(a), _ptr(b), _ptr(c), _ptr(ebuf), m, n, k, k, n, n,
+                                          float(alpha), float(beta), flags, cp, _ptr(ws), need,
+                                          ctypes.c_void_p(sh)))
     return c
 
 
@@ -275,9 +315,27 @@ def bias_relu_(y: torch.Tensor, bias: torch.Tensor | None, relu: bool = True,
     GPU baseline of the fused epilogue, and the stand-alone element-wise nest)."""
     _need_cuda_f32("y", y)
     n, kt, p, q, v = y.shape
-    flags, bias = _epilogue(bias, relu, relu6, scale, kt * 16)
-    check(lib().pdl_bias_relu_nchw16c(_ptr(y), _ptr(bias), n, kt * 16, p, q, flags,
-                                      ctypes.c_void_p(_stream(stream))))
+    with _on(stream):
+        flags, bias = _epilogue(bias, relu, relu6, scale, kt * 16)
+        check(lib().pdl_bias_relu_nchw16c(_ptr(y), _ptr(bias), n, kt * 16, p, q, flags,
+                                          ctypes.c_void_p(_stream(stream))))
+    return y
+
+
+def accumulate_(y: torch.Tensor, y0: torch.Tensor, bias: torch.Tensor | None = None,
+                relu: bool = False, stream=None, relu6: bool = False,
+                scale: torch.Tensor | None = None) -> torch.Tensor:
+    """y = act((y + y0) * scale + bias) in place over nKhw16k: a convolution's `+=`
+    onto incoming output contents y0, with the nest's element-wise epilogue."""
+    _need_cuda_f32("y", y)
+    _need_cuda_f32("y0", y0)
+    if y0.shape != y.shape:
+        raise ValueError(f"y0 {tuple(y0.shape)} != y {tuple(y.shape)}")
+    n, kt, p, q, v = y.shape
+    with _on(stream):
+        flags, bias = _epilogue(bias, relu, relu6, scale, kt * 16)
+        check(lib().pdl_accumulate_epilogue_nchw16c(_ptr(y), _ptr(y0), _ptr(bias), n, kt * 16, p, q,
+                                                    flags, ctypes.c_void_p(_stream(stream))))
     return y
 
 
@@ -320,17 +378,19 @@ def conv2d_nchw(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = No
     """PyTorch-layout convenience: NCHW x, OIHW w -> NCHW y, through pack ->
     blocked conv (+bias, +ReLU) -> unpack; all on the GPU."""
     c = x.shape[1]
-    xb = to_nchw16c(x, stream=stream)
-    pw = prepack_weights(weights_to_kcrs16c16k(w, stream=stream), mode=mode, channels=c, stream=stream)
-    yb = conv2d_nchw16c(xb, pw, bias, stride=stride, pad=pad, relu=relu, mode=mode, cfg=cfg,
-                        channels=c, stream=stream)
-    return from_nchw16c(yb, w.shape[0], stream=stream)
+    with _on(stream):   # the intermediates xb / pw / yb live (and die) on `stream`
+        xb = to_nchw16c(x, stream=stream)
+        pw = prepack_weights(weights_to_kcrs16c16k(w, stream=stream), mode=mode, channels=c,
+                             stream=stream)
+        yb = conv2d_nchw16c(xb, pw, bias, stride=stride, pad=pad, relu=relu, mode=mode, cfg=cfg,
+                            channels=c, stream=stream)
+        return from_nchw16c(yb, w.shape[0], stream=stream)
 
 
 def device_ok() -> bool:
     return lib().pdl_device_check() == 0
 
 
-__all__ = ["conv2d_nchw16c", "prepack_weights", "PackedWeights", "gemm", "bias_relu_",
-           "device_ok", "conv_out_hw", "TileCfg"]
+__all__ = ["conv2d_nchw16c", "prepack_weights", "PackedWeights", "gemm", "bias_relu_", "accumulate_",
+           "device_ok", "conv_out_hw", "TileCfg", "SimtPathWarning"]
 _ = _lib

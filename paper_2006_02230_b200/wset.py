@@ -208,7 +208,9 @@ def working_sets(nest: LoopNest, binding: Mapping[str, int], sample_outer: bool 
                 dep_id = f"{src}->{tgt}"
                 common = [p for p in tr.par_iters[s_label] if p in tr.par_iters[t_label]]
                 if common and _spans(tr, pos, by_label, src, tgt, common):
-                    ws = _par_footprint(tr, by_label, common[0], sample_outer)
+                    # over the SOURCE statement's outermost parallel iterator, as the
+                    # reference's classify_parallel_span reports it (depend.py:158-159)
+                    ws = _par_footprint(tr, by_label, tr.par_iters[s_label][0], sample_outer)
                     entries.append(WorkingSetEntry(dep_id, kind, array, "par", ws))
                     continue
                 key = lambda t: inst[t][1]  # counters: lexicographic order of iteration vectors

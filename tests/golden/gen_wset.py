@@ -61,6 +61,23 @@ st: for (t = 0; t < T; t++) {
 }
 """
 
+# Sibling parallel loops under one sequential loop, the iterator name `i` reused: the
+# S1 -> S2 dependence spans the common parallel iterator i, and WS_par is taken over
+# the SOURCE statement's outermost parallel iterator p (reference depend.py:158-159).
+SIBLING_PAR = """param N;
+array a[N][N]; array b[N];
+t: for (s = 0; s < 2; s++) {
+  parallel for (p = 0; p < 2; p++) {
+    parallel for (i = 0; i < N; i++) {
+      S1: a[p][i] = b[i] * 2.0;
+    }
+  }
+  parallel for (i = 0; i < N; i++) {
+    S2: b[i] = a[0][N - 1 - i] + 1.0;
+  }
+}
+"""
+
 CASES = [
     ("gemm_seq_333", GEMM.format(par=""), {"M": 3, "N": 3, "K": 3}),
     ("gemm_seq_444", GEMM.format(par=""), {"M": 4, "N": 4, "K": 4}),
@@ -74,6 +91,7 @@ CASES = [
      {"N": 1, "KT": 1, "CT": 1, "P": 2, "Q": 2, "R": 3, "S": 3}),
     ("conv_1x1_s2_tiny", conv_pdl(2, False).replace("16", "2"),
      {"N": 1, "KT": 1, "CT": 1, "P": 2, "Q": 2, "R": 1, "S": 1}),
+    ("sibling_par_4", SIBLING_PAR, {"N": 4}),
 ]
 
 
@@ -102,8 +120,16 @@ def _run(text, binding, q):
 
 
 def main():
+    """`--only NAME ...` regenerates just those cases, keeping the others' records."""
+    only = sys.argv[sys.argv.index("--only") + 1:] if "--only" in sys.argv else None
     out = {"generator": "looprank.wset.working_sets (reference, unmodified)", "cases": []}
+    if only:
+        with open(os.path.join(HERE, "wset_ref.json")) as fh:
+            out = json.load(fh)
+        out["cases"] = [c for c in out["cases"] if c["name"] not in only]
     for name, text, binding in CASES:
+        if only and name not in only:
+            continue
         q = mp.Queue()
         p = mp.Process(target=_run, args=(text, binding, q))
         p.start()

@@ -39,7 +39,10 @@ def test_interpret_reference_program(path):
     prog = L.parse_program(str(g["text"]))
     binding, inputs = conv_case(g)
     arrays, trace = P.interpret(prog, binding, inputs=inputs)
-    assert trace is None
+    from paper_2006_02230_b200.trace import LazyTrace
+    assert isinstance(trace, tuple) and len(trace) == len(prog.nests)
+    assert all(isinstance(t, LazyTrace) for t in trace)
+    assert P.interpret(prog, binding, inputs=inputs, collect_trace=False)[1] is None
     assert rel(arrays["output"].reshape(g["y"].shape), g["y"]) <= 1e-5
     np.testing.assert_array_equal(arrays["filter"], np.asarray(g["w"], np.float64).ravel())
 
@@ -51,9 +54,10 @@ def test_interpret_reference_gemm(path):
     g = np.load(path)
     nest = L.parse(str(g["text"]))
     m, n, k = int(g["M"]), int(g["N"]), int(g["K"])
-    arrays, _ = P.interpret(nest, dict(M=m, N=n, K=k),
-                            inputs={"A": g["A"], "B": g["B"], "C": np.zeros(m * n)})
+    arrays, trace = P.interpret(nest, dict(M=m, N=n, K=k),
+                                inputs={"A": g["A"], "B": g["B"], "C": np.zeros(m * n)})
     assert rel(arrays["C"].reshape(m, n), g["C"]) <= 1e-5
+    assert len(trace) == 4 * m * n * k   # A, B, C reads + C write per MAC (simcache.py:193-198)
 
 
 def test_accumulate_into_nonzero_output_and_tiled_variant():
