@@ -59,13 +59,17 @@ typedef struct pdl_tile_cfg {
     int cluster_n; /* 2: CTA-pair tiles, cta_group::2 MMAs with M = 256 (3xTF32 conv) */
     int split_k;   /* 0: auto (split the reduction when the tiles leave SMs idle
                       and a workspace is given), 1: off, >1: that many ranges   */
-    int raster;    /* bit 0: reserved (tile order); bit 1 (PDL_RASTER_BOX_TILES):
+    int raster;    /* bit 0 (PDL_RASTER_M_FASTEST): tile order with output-pixel tiles
+                      fastest (consecutive CTAs share weights; default: output-channel
+                      tiles fastest, they share activations; ignored with clusters,
+                      CTA pairs, the stem and resident weights); bit 1 (PDL_RASTER_BOX_TILES):
                       box tiles only -- no multi-image segment tiles for small maps;
                       bit 2 (PDL_RASTER_SEG_TILES): segment tiles whenever the shape
                       allows, even if they do not remove a wave of tiles; bits 4
                       and 6 below; any other bit: PDL_EUNSUPPORTED              */
 } pdl_tile_cfg;
 
+#define PDL_RASTER_M_FASTEST 1
 #define PDL_RASTER_BOX_TILES 2
 #define PDL_RASTER_SEG_TILES 4
 #define PDL_RASTER_NO_HALO 16  /* 3x3 convs: one A box per tap instead of one halo per channel group */
@@ -211,6 +215,32 @@ int pdl_unpack_nchw16c(const float *src, float *dst, int N, int C, int H, int W,
 int pdl_pack_kcrs16c16k(const float *src, float *dst, int K, int C, int R, int S, void *stream);
 
 size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg);
+
+/* The schedule the library will run for a call (after its own rules: resident
+ * weights, halo mode, segment tiles, split-K planning, 256-column TF32 tiles) --
+ * what the ranker reasons about.  Pure host computation; no device work. */
+typedef struct pdl_schedule {
+    int kind;        /* 1: tile-engine conv, 2: narrow-channel stem conv, 3: GEMM        */
+    int bn, bk;      /* output columns per tile; reduction elements per k-block          */
+    int cluster;     /* CTAs per cluster (2 with a CTA pair)                              */
+    int tile_w, tile_h, tile_images; /* output pixels per M tile (GEMM: 128 x 1 x 1)     */
+    int seg_rows;    /* > 0: segment tiles of that many output rows (bands)               */
+    int m_tiles, n_tiles;
+    int num_kb;      /* k-blocks per tile                                                 */
+    int split, kb_per; /* split-K ranges per tile, k-blocks per range                     */
+    int halo;        /* input halo loaded once per channel group (stem: whole-tile halo)  */
+    int resident;    /* weights of the N-tile resident in shared memory                   */
+    int pair;        /* CTA pair (cta_group::2, M = 256)                                  */
+    int order;       /* 1: output-pixel tiles fastest                                     */
+    int flat;        /* 1x1 / stride 1 / pad 0 map flattened to one row                   */
+    size_t splitk_workspace_bytes;
+} pdl_schedule;
+/* with_workspace != 0: the call will pass a split-K workspace (auto split may engage). */
+int pdl_conv2d_schedule(int N, int C, int K, int H, int W, int R, int S, int stride, int pad,
+                        unsigned flags, const pdl_tile_cfg *cfg, int with_workspace,
+                        pdl_schedule *out);
+int pdl_gemm_schedule(int M, int N, int K, unsigned flags, const pdl_tile_cfg *cfg,
+                      int with_workspace, pdl_schedule *out);
 
 /* Tile config the library would pick for a conv / GEMM (for the ranker and
  * the bench's roofline report).  Writes *cfg, returns 0. */

@@ -7,8 +7,9 @@ Kernels live in libpdl.so (csrc/, C ABI in include/pdl.h); there is no CPU
 fallback on this path.
 """
 from ._lib import PdlDeviceError, PdlError, PdlShapeError, TileCfg  # noqa: F401
-from .ops import (PackedWeights, bias_relu_, conv2d_nchw, conv2d_nchw16c, conv2d_nchw16c_host,  # noqa: F401
-                  conv_out_hw,
+from . import ops  # noqa: F401
+from .ops import (PackedWeights, SimtPathWarning, accumulate_, bias_relu_, conv2d_nchw,  # noqa: F401
+                  conv2d_nchw16c, conv2d_nchw16c_host, conv_out_hw,
                   device_ok, from_nchw16c, gemm, prepack_weights, to_nchw16c,
                   weights_to_kcrs16c16k)
 

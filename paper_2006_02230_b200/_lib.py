@@ -39,7 +39,7 @@ EXPORTS = (
     "pdl_abi_version", "pdl_device_check", "pdl_pack_nchw16c", "pdl_unpack_nchw16c",
     "pdl_pack_kcrs16c16k", "pdl_conv2d_host_workspace_bytes", "pdl_conv2d_fwd_host",
     "pdl_conv2d_splitk_workspace_bytes", "pdl_conv2d_fwd_prepacked_ws", "pdl_gemm_f32_epilogue",
-    "pdl_accumulate_epilogue_nchw16c",
+    "pdl_accumulate_epilogue_nchw16c", "pdl_conv2d_schedule", "pdl_gemm_schedule",
 )
 
 
@@ -74,6 +74,17 @@ class TileCfg(ctypes.Structure):
         return c
 
 
+class Schedule(ctypes.Structure):
+    """pdl_schedule (include/pdl.h): the schedule the library will actually run."""
+    _fields_ = [(n, ctypes.c_int) for n in
+                ("kind", "bn", "bk", "cluster", "tile_w", "tile_h", "tile_images", "seg_rows",
+                 "m_tiles", "n_tiles", "num_kb", "split", "kb_per", "halo", "resident", "pair",
+                 "order", "flat")] + [("splitk_workspace_bytes", ctypes.c_size_t)]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -83,7 +94,33 @@ _u = ctypes.c_uint
 _sz = ctypes.c_size_t
 
 
+# Entry points an older build may lack (PDL_LIB A/B runs against a previous round's
+# library): declared only when present.
+_OPTIONAL = ("pdl_gemm_f32_epilogue", "pdl_accumulate_epilogue_nchw16c", "pdl_conv2d_schedule",
+             "pdl_gemm_schedule")
+
+
+class _Skip:
+    """Stand-in for a missing optional symbol while declaring (attribute writes vanish)."""
+    def __setattr__(self, k, v):
+        pass
+
+
+class _Tolerant:
+    def __init__(self, L):
+        object.__setattr__(self, "_L", L)
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._L, name)
+        except AttributeError:
+            if name in _OPTIONAL and os.environ.get("PDL_LIB"):
+                return _Skip()
+            raise
+
+
 def _declare(L):
+    L = _Tolerant(L)
     L.pdl_conv2d_fwd_nchw16c.argtypes = [_vp, _vp, _vp, _vp] + [_i] * 9 + [
         _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
     L.pdl_conv2d_packed_bytes.argtypes = [_i, _i, _i, _i, _u]
@@ -105,6 +142,8 @@ def _declare(L):
         ctypes.c_float, ctypes.c_float, _u, ctypes.POINTER(TileCfg), _vp, _sz, _vp]
     L.pdl_bias_relu_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _u, _vp]
     L.pdl_accumulate_epilogue_nchw16c.argtypes = [_vp, _vp, _vp, _i, _i, _i, _i, _u, _vp]
+    L.pdl_conv2d_schedule.argtypes = [_i] * 9 + [_u, ctypes.POINTER(TileCfg), _i, ctypes.POINTER(Schedule)]
+    L.pdl_gemm_schedule.argtypes = [_i, _i, _i, _u, ctypes.POINTER(TileCfg), _i, ctypes.POINTER(Schedule)]
     L.pdl_pack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_unpack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_pack_kcrs16c16k.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
@@ -153,6 +192,22 @@ def default_cfg(op: int, dims) -> TileCfg:
     c = TileCfg()
     check(lib().pdl_default_cfg(op, arr, ctypes.byref(c)))
     return c
+
+
+def conv_schedule(N, C, K, H, W, R, S, stride, pad, flags, cfg=None, with_workspace=True) -> dict:
+    """The schedule libpdl runs for this conv call (host-only; works without a GPU)."""
+    out = Schedule()
+    cp = None if cfg is None else ctypes.byref(cfg if isinstance(cfg, TileCfg) else TileCfg.make(**cfg))
+    check(lib().pdl_conv2d_schedule(N, C, K, H, W, R, S, stride, pad, flags, cp, int(with_workspace),
+                                    ctypes.byref(out)))
+    return out.as_dict()
+
+
+def gemm_schedule(M, N, K, flags, cfg=None, with_workspace=True) -> dict:
+    out = Schedule()
+    cp = None if cfg is None else ctypes.byref(cfg if isinstance(cfg, TileCfg) else TileCfg.make(**cfg))
+    check(lib().pdl_gemm_schedule(M, N, K, flags, cp, int(with_workspace), ctypes.byref(out)))
+    return out.as_dict()
 
 
 def last_launch_count() -> int:

@@ -145,7 +145,7 @@ constexpr unsigned kDiag = 0;
 constexpr unsigned kEpiFlags = PDL_BIAS | PDL_RELU | PDL_RELU6 | PDL_SCALE;
 constexpr unsigned kConvFlags = kEpiFlags | PDL_MODE_MASK;
 constexpr unsigned kGemmFlags = kEpiFlags | PDL_MODE_MASK | PDL_NO_SIMT;
-constexpr int kRasterBits = 1 | PDL_RASTER_BOX_TILES | PDL_RASTER_SEG_TILES | PDL_RASTER_NO_HALO | PDL_RASTER_HALO_CG4;
+constexpr int kRasterBits = PDL_RASTER_M_FASTEST | PDL_RASTER_BOX_TILES | PDL_RASTER_SEG_TILES | PDL_RASTER_NO_HALO | PDL_RASTER_HALO_CG4;
 
 int check_flags(unsigned flags, unsigned allowed, const char *what) {
     const unsigned bad = flags & ~(allowed | kDiag);
@@ -568,6 +568,27 @@ int conv_check(const float *x, const float *y, int N, int C, int K, int H, int W
     return PDL_OK;
 }
 
+// Stem tile = BW x BH output pixels (<= 128); its input halo (box_w x box_h pixels,
+// 16 B each) is one TMA box and one pipeline stage.  Per tile the engine spends
+// ~R x 700 cycles on MMAs and the TMA ~4.4 cycles per 16-byte halo element (both
+// measured on B200, profiles/trace_*); pick the shape minimising tiles x max(the two).
+bool stem_tile(int P, int Q, int R, int S, int stride, int *BWo, int *BHo) {
+    constexpr double kMmaPerRow = 700.0, kTmaPerElem = 4.4;
+    double best = 1e30;
+    int BW = 0, BH = 0;
+    for (int bw = std::min(Q, 128); bw >= 1; --bw) {
+        const int bh = std::min(P, 128 / bw);
+        const int bxw = (bw - 1) * stride + S, bxh = (bh - 1) * stride + R;
+        if (bxw > 256 || bxh > 256 || 16 * bxw * bxh > pdl::kStemHaloBytes) continue;
+        const double tiles = (double)((Q + bw - 1) / bw) * ((P + bh - 1) / bh);
+        const double cost = tiles * std::max(R * kMmaPerRow, kTmaPerElem * bxw * bxh);
+        if (cost < best - 1e-9) { best = cost; BW = bw; BH = bh; }
+    }
+    *BWo = BW;
+    *BHo = BH;
+    return BW > 0;
+}
+
 int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, int N, int C,
                   int K, int H, int W, int R, int S, int stride, int pad, unsigned flags,
                   const pdl_tile_cfg *cfg_in, cudaStream_t st) {
@@ -582,19 +603,8 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     // (both measured on B200, profiles/trace_*); pick the shape minimising
     // tiles x max(the two).
     int BW = 0, BH = 0;
-    {
-        constexpr double kMmaPerRow = 700.0, kTmaPerElem = 4.4;
-        double best = 1e30;
-        for (int bw = std::min(Q, 128); bw >= 1; --bw) {
-            const int bh = std::min(P, 128 / bw);
-            const int bxw = (bw - 1) * stride + S, bxh = (bh - 1) * stride + R;
-            if (bxw > 256 || bxh > 256 || 16 * bxw * bxh > pdl::kStemHaloBytes) continue;
-            const double tiles = (double)((Q + bw - 1) / bw) * ((P + bh - 1) / bh);
-            const double cost = tiles * std::max(R * kMmaPerRow, kTmaPerElem * bxw * bxh);
-            if (cost < best - 1e-9) { best = cost; BW = bw; BH = bh; }
-        }
-        if (!BW) return fail(PDL_EUNSUPPORTED, "stem: no halo tile fits (S=%d R=%d)", S, R);
-    }
+    if (!stem_tile(P, Q, R, S, stride, &BW, &BH))
+        return fail(PDL_EUNSUPPORTED, "stem: no halo tile fits (S=%d R=%d)", S, R);
     int box_w = (BW - 1) * stride + S;
     const int box_h = (BH - 1) * stride + R;
     // packed stride-2 stem: the halo is loaded as two dense boxes, even and odd input
@@ -678,12 +688,32 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
 int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, int N, int C, int K,
                 int H, int W, int R, int S, int stride, int pad, unsigned flags,
                 const pdl_tile_cfg *cfg_in, cudaStream_t st, void *ws = nullptr, size_t ws_bytes = 0,
-                size_t *query = nullptr) {
+                size_t *query = nullptr, pdl_schedule *sched = nullptr) {
     int rc;
     if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
     if (is_stem(C, R, S, stride)) {
         if (query) {
             *query = 0;
+            return PDL_OK;
+        }
+        if (sched) {
+            const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+            int BW, BH;
+            if (!stem_tile(P, Q, R, S, stride, &BW, &BH)) return fail(PDL_EUNSUPPORTED, "stem: no halo tile fits");
+            std::memset(sched, 0, sizeof(*sched));
+            sched->kind = 2;
+            sched->bn = 64;
+            sched->bk = 4 * stem_chunks_per_kb(C, R, S);
+            sched->cluster = 1;
+            sched->tile_w = BW;
+            sched->tile_h = BH;
+            sched->tile_images = 1;
+            sched->m_tiles = ((Q + BW - 1) / BW) * ((P + BH - 1) / BH) * N;
+            sched->n_tiles = (K + 63) / 64;
+            sched->num_kb = sched->kb_per = stem_kblocks(C, R, S);
+            sched->split = 1;
+            sched->resident = 1;
+            sched->halo = 1;
             return PDL_OK;
         }
         if ((rc = get_encode())) return rc;
@@ -746,10 +776,6 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         *query = spl.bytes;
         return PDL_OK;
     }
-    if ((rc = get_encode())) return rc;
-
-    pdl::TmaMaps maps;
-    std::memset(&maps, 0, sizeof(maps));
     // halo mode (3xTF32, stride 1, spatial filter): one box of the tile's whole input halo
     // per channel group instead of one box per tap
     // 3xTF32 64-channel k-blocks at BN=64 (layer 3) take halo mode with one halo buffer:
@@ -764,6 +790,33 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                       (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
                       !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
+    if (sched) {
+        std::memset(sched, 0, sizeof(*sched));
+        sched->kind = 1;
+        sched->bn = cfg.bn;
+        sched->bk = cfg.bk;
+        sched->cluster = pair ? 2 : cl;
+        sched->tile_w = g.seg_mode ? g.Q * g.seg_imgs : g.BW;
+        sched->tile_h = g.seg_mode ? g.seg_tile : g.BH;
+        sched->tile_images = g.seg_mode ? g.seg_imgs : g.BNI;
+        sched->seg_rows = g.seg_mode ? g.seg_tile : 0;
+        sched->m_tiles = m_tiles;
+        sched->n_tiles = n_tiles;
+        sched->num_kb = num_kb;
+        sched->split = spl.split;
+        sched->kb_per = spl.kb_per;
+        sched->halo = halo ? 1 : 0;
+        sched->resident = resident ? 1 : 0;
+        sched->pair = pair ? 1 : 0;
+        sched->order = (cl == 1 && !pair && !resident) ? (cfg.raster & 1) : 0;
+        sched->flat = g.flat ? 1 : 0;
+        sched->splitk_workspace_bytes = spl.bytes;
+        return PDL_OK;
+    }
+    if ((rc = get_encode())) return rc;
+
+    pdl::TmaMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
     cuuint32_t abox[5] = {16, (cuuint32_t)g.BW, (cuuint32_t)g.BH, 1, (cuuint32_t)g.BNI};
     if (halo) {
         abox[1] = (cuuint32_t)halo_w;
@@ -863,7 +916,9 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     p.seg_bytes = g.Q * g.seg_imgs * 64;
     p.seg_imgs = g.seg_imgs;
     p.m_tiles = m_tiles;
-    p.raster = cfg.raster;
+    // tile order (raster bit 0) only where CTAs do not pin an N-tile: no clusters, pairs,
+    // resident weights
+    p.raster = (cl == 1 && !pair && !resident) ? (cfg.raster & 1) : 0;
     p.n_tiles = n_tiles;
     if ((rc = bind_split(p, spl, ws, ws_bytes, cl))) return rc;
     if (halo) {
@@ -1032,6 +1087,18 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
     if (!aligned16(packed_w)) return fail(PDL_EALIGN, "conv: packed weights unaligned");
     return conv_fwd_tc(x, reinterpret_cast<const float *>(packed_w), bias, y, N, C, K, H, W, R, S,
                        stride, pad, flags, cfg, (cudaStream_t)stream, workspace, ws_bytes);
+}
+
+int pdl_conv2d_schedule(int N, int C, int K, int H, int W, int R, int S, int stride, int pad,
+                        unsigned flags, const pdl_tile_cfg *cfg, int with_workspace, pdl_schedule *out) {
+    int rc;
+    if (!out) return fail(PDL_EINVAL, "schedule: null output");
+    if ((rc = check_flags(flags, kConvFlags, "schedule"))) return rc;
+    if ((rc = conv_check(nullptr, nullptr, N, C, K, H, W, R, S, stride, pad))) return rc;
+    // a non-null stand-in workspace: auto split-K may engage
+    static char ws_token;
+    return conv_fwd_tc(nullptr, nullptr, nullptr, nullptr, N, C, K, H, W, R, S, stride, pad, flags, cfg,
+                       nullptr, with_workspace ? &ws_token : nullptr, 0, nullptr, out);
 }
 
 size_t pdl_conv2d_host_workspace_bytes(int N, int C, int K, int H, int W, int R, int S, int stride,
@@ -1253,7 +1320,7 @@ int pdl_gemm_f32_epilogue(const float *A, const float *B, float *C, const float 
     p.ldc = ldc;
     p.alpha = alpha;
     p.beta = beta;
-    p.raster = raster;
+    p.raster = cl == 1 ? (raster & 1) : 0;
     p.m_tiles = (M + 127) / 128;
     p.n_tiles = (N + bn - 1) / bn;
     {
@@ -1267,6 +1334,36 @@ int pdl_gemm_f32_epilogue(const float *A, const float *B, float *C, const float 
                                        : dispatch_epix<pdl::KIND_GEMM, false>(bn, 1, maps, p, st);
     if (mode == PDL_MODE_3XTF32) return dispatch_tile<pdl::KIND_GEMM, true>(bn, 1, cl, maps, p, st);
     return dispatch_tile<pdl::KIND_GEMM, false>(bn, 1, cl, maps, p, st);
+}
+
+int pdl_gemm_schedule(int M, int N, int K, unsigned flags, const pdl_tile_cfg *cfg_in, int with_workspace,
+                      pdl_schedule *out) {
+    int rc;
+    if (!out) return fail(PDL_EINVAL, "schedule: null output");
+    if ((rc = check_flags(flags, kGemmFlags, "schedule"))) return rc;
+    if (M <= 0 || N <= 0 || K <= 0) return fail(PDL_EINVAL, "schedule: non-positive GEMM dimension");
+    int bn, cl, raster;
+    gemm_cfg(M, N, cfg_in, &bn, &cl, &raster);
+    if (flags & (PDL_RELU6 | PDL_SCALE)) cl = 1;
+    std::memset(out, 0, sizeof(*out));
+    out->kind = 3;
+    out->bn = bn;
+    out->bk = 32;
+    out->cluster = cl;
+    out->tile_w = 128;
+    out->tile_h = out->tile_images = 1;
+    out->m_tiles = (M + 127) / 128;
+    out->n_tiles = (N + bn - 1) / bn;
+    out->num_kb = (K + 31) / 32;
+    const int req = cfg_in ? cfg_in->split_k : 0;
+    const SplitPlan spl = plan_split(out->m_tiles, out->n_tiles, cl, bn, out->num_kb, kSegElems / 32,
+                                     with_workspace ? req : (req > 1 ? req : 1));
+    out->split = spl.split;
+    out->kb_per = spl.kb_per;
+    out->order = cl == 1 ? (raster & 1) : 0;
+    out->flat = 1;
+    out->splitk_workspace_bytes = spl.bytes;
+    return PDL_OK;
 }
 
 int pdl_gemm_f32(const float *A, const float *B, float *C, int M, int N, int K, int lda, int ldb,

@@ -83,7 +83,7 @@ struct TileParams {
     int res_bytes;         // resident-weight conv: bytes of one weight plane of the N-tile
     int m_tiles;           // number of M tiles
     int n_tiles;           // number of N tiles
-    int raster;            // reserved
+    int raster;            // bit 0: M-tiles fastest tile order (see tile_coord)
     int seg_kb;            // k-blocks per TMEM accumulation segment
     // split-K: every tile's reduction is cut into `split` ranges of kb_per k-blocks,
     // computed as separate work units; each writes its fp32 partial to part, and the
@@ -398,8 +398,18 @@ struct TileCoord {
 template <int KIND, int BN>
 __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     TileCoord c;
-    const int mt = tile / p.n_tiles;
-    c.n0 = (tile - mt * p.n_tiles) * BN;
+    // raster bit 0: M-tiles fastest (consecutive CTAs share a weight N-tile through L2);
+    // default N-tiles fastest (they share activation rows).  The host clears the bit for
+    // the stem, resident-weight tiles and clusters (one N-tile per CTA / cluster lockstep).
+    int mt, nt;
+    if (p.raster & 1) {
+        nt = tile / p.m_tiles;
+        mt = tile - nt * p.m_tiles;
+    } else {
+        mt = tile / p.n_tiles;
+        nt = tile - mt * p.n_tiles;
+    }
+    c.n0 = nt * BN;
     c.m0 = 0;
     c.q0 = 0;
     c.p0 = 0;
@@ -905,7 +915,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (SPLIT3) tmem_st16(t_hi + G::KS + c * 16, lo);
                             }
                         }
-                        if (kb + 1 == p.num_kb) mbar_arrive(&empty[s]);  // halo tile consumed
+                        if (kb + 1 == p.num_kb) {  // halo tile consumed
+                            fence_proxy_async_smem();
+                            mbar_arrive(&empty[s]);
+                        }
                         tmem_wait_st();
                         tc_fence_before();
                         mbar_arrive(&tready[t]);
@@ -920,7 +933,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (live && tp < p.S) v = lds128(sa + kb * row_step + tp * 16);
                         x[4 * tp] = v.x; x[4 * tp + 1] = v.y; x[4 * tp + 2] = v.z; x[4 * tp + 3] = v.w;
                     }
-                    if (kb + 1 == p.num_kb) mbar_arrive(&empty[s]);  // halo tile consumed
+                    if (kb + 1 == p.num_kb) {  // halo tile consumed
+                        fence_proxy_async_smem();
+                        mbar_arrive(&empty[s]);
+                    }
 #pragma unroll
                     for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
                     mbar_wait(&tfree[t], tph ^ 1);
@@ -1010,6 +1026,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     x[16 * c + 4 * j + 2] = v.z; x[16 * c + 4 * j + 3] = v.w;
                                 }
                             if (group_end) {  // every tap of this channel group has been read
+                                // the next TMA (async proxy) write of this buffer must not
+                                // overtake these generic-proxy reads (measured: without the
+                                // fence, halo + short split-K ranges read a reloaded buffer)
+                                fence_proxy_async_smem();
                                 mbar_arrive(&hempty[hb]);
                                 if (++hb == L::HALO_NBUF) { hb = 0; hph ^= 1; }
                             }
@@ -1023,6 +1043,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     x[16 * c + 4 * j] = v.x; x[16 * c + 4 * j + 1] = v.y;
                                     x[16 * c + 4 * j + 2] = v.z; x[16 * c + 4 * j + 3] = v.w;
                                 }
+                            fence_proxy_async_smem();  // generic reads before the stage's next TMA write
                             mbar_arrive(&empty[s]);  // A rows read
                         }
                         mbar_wait(&tfree[t], tph ^ 1);

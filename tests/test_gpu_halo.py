@@ -56,22 +56,6 @@ def test_halo_bitwise_equals_per_tap_boxes(P, case, split, mode):
     assert rel(halo.cpu().numpy(), ref) <= (1e-5 if mode == "3xtf32" else 1e-2)
 
 
-@pytest.mark.parametrize("case", [c for c in CASES if c[0] >= 128] + [(48, 32, 9, 3, 3)],
-                         ids=lambda c: "c%dk%dh%dr%dn%d" % c)
-def test_weights_lo_on_chip_bitwise(P, case):
-    """PDL_RASTER_BLO_ONCHIP: only the weights' hi plane is loaded and the staging
-    warps form lo = w - tf32(w) in shared memory -- the same value the prepack stores."""
-    C, K, H, R, N = case
-    layer = W.ConvLayer(0, C, K, H, R, 1)
-    x, w, b = W.conv_inputs(layer, N, seed=37)
-    pw = P.prepack_weights(torch.from_numpy(w).cuda())
-    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
-    kw = dict(stride=1, pad=R // 2, relu=True)
-    a = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 1, "cluster_m": 1}, **kw)
-    c = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 1, "cluster_m": 1, "raster": 32}, **kw)
-    assert torch.equal(a, c)
-
-
 def test_halo_single_buffer_64_channel_kblocks(P):
     """PDL_RASTER_HALO_CG4: 3xTF32 halo with 64-channel k-blocks and one halo buffer."""
     for case in [(64, 64, 56, 3, 2), (128, 64, 14, 3, 3)]:

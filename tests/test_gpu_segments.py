@@ -73,22 +73,23 @@ def test_resnet_small_map_layers_full_batch_sample(P):
             assert rel(yn[i:i + 1], ref) <= 1e-5, layer.name()
 
 
-LSU = 8  # PDL_RASTER_LSU_EPI
-
-
 @pytest.mark.parametrize("case", [(64, 256, 56, 1, 1, 2), (128, 128, 28, 3, 1, 3), (256, 128, 28, 1, 2, 2),
-                                  (512, 512, 7, 3, 1, 3), (48, 32, 9, 3, 2, 3), (3, 64, 40, 7, 2, 2)],
+                                  (512, 512, 7, 3, 1, 3), (48, 32, 9, 3, 2, 3), (3, 64, 40, 7, 2, 2),
+                                  (256, 1024, 14, 1, 1, 4)],
                          ids=lambda c: "c%dk%dh%dr%ds%dn%d" % c)
-def test_lsu_epilogue_bitwise_equals_tma(P, case):
-    """The coalesced LSU epilogue (warp-local transpose + st.global.v4) stores the
-    same values as the TMA box stores, including clipped pixels at map edges."""
+@pytest.mark.parametrize("split", [1, 3])
+def test_m_fastest_tile_order_bitwise(P, case, split):
+    """PDL_RASTER_M_FASTEST (raster bit 0, the tile-loop interchange of the variant
+    space): output-pixel tiles fastest instead of output-channel tiles.  Every tile
+    reduces in the same order, so results are bitwise equal (segment, box and
+    split-K tiles; silently ignored where CTAs pin an N-tile: stem, resident weights)."""
     C, K, H, R, stride, N = case
     layer = W.ConvLayer(0, C, K, H, R, stride)
     x, w, b = W.conv_inputs(layer, N, seed=23)
     pw = P.prepack_weights(torch.from_numpy(w).cuda(), channels=C)
     xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
     kw = dict(stride=stride, pad=R // 2, relu=True)
-    tma = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 1, "raster": BOX}, **kw)
-    sentinel = torch.full_like(tma, float("nan"))
-    lsu = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 1, "raster": BOX | LSU}, out=sentinel, **kw)
-    assert torch.equal(tma, lsu)
+    n_first = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": split}, **kw)
+    sentinel = torch.full_like(n_first, float("nan"))
+    m_first = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": split, "raster": 1}, out=sentinel, **kw)
+    assert torch.equal(n_first, m_first)

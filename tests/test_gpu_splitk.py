@@ -111,3 +111,40 @@ def test_gemm_splitk_vs_oracle(P, mnk, split):
            cfg={"split_k": split})
     ref = 0.5 * oracle.gemm_f64(a, bm) - 2.0 * c0.astype(np.float64)
     assert rel(c.cpu().numpy(), ref) <= 1e-5
+
+
+# Halo mode + short split-K ranges, repeated: the staging warps' generic-proxy reads of a
+# halo buffer must be fenced (fence.proxy.async) before the buffer is released to the
+# next TMA write.  Without the fence a 1-k-block range re-loaded the buffer while a warp
+# still read the last tap (wrong rows in ~1 of 4 launches).  Every repetition must be
+# bitwise equal to the first and within the mode's bar of the unsplit schedule.
+RACE = [  # (C, K, H, R, N, mode, extra cfg, splits)
+    (64, 64, 56, 3, 1, "3xtf32", {"bk": 32}, (18, 19, 24)),    # PR1, 1-k-block ranges
+    (64, 64, 56, 3, 1, "tf32", {"bk": 32}, (18, 19)),
+    (512, 512, 7, 3, 32, "tf32", {}, (3, 4, 6, 9)),             # layer 17, 8-image shard
+    (512, 512, 7, 3, 32, "3xtf32", {}, (9, 12, 18)),
+    (256, 256, 14, 3, 8, "3xtf32", {}, (15, 16, 21)),           # layer 12
+    (64, 64, 56, 3, 2, "3xtf32", {}, (13, 18)),                 # layer 3
+]
+
+
+@pytest.mark.parametrize("case", RACE, ids=lambda c: "c%dk%dh%dr%dn%d_%s" % c[:6])
+def test_halo_splitk_repeated_launches_are_identical(P, case):
+    C, K, H, R, N, mode, extra, splits = case
+    layer = W.ConvLayer(0, C, K, H, R, 1)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(C + K + N)
+    x = torch.rand((N, C // 16, H, H, 16), generator=g, device="cuda") * 2 - 1
+    w = torch.rand((K // 16, C // 16, R, R, 16, 16), generator=g, device="cuda") * 2 - 1
+    pw = P.prepack_weights(w, mode=mode)
+    base = P.conv2d_nchw16c(x, pw, stride=1, pad=R // 2, mode=mode, cfg=dict(extra, split_k=1))
+    scale = float(base.abs().max())
+    tol = 1e-5 if mode == "3xtf32" else 1e-3
+    for s in splits:
+        cfg = dict(extra, split_k=s)
+        first = P.conv2d_nchw16c(x, pw, stride=1, pad=R // 2, mode=mode, cfg=cfg)
+        assert float((first - base).abs().max()) <= tol * scale, (s, "vs unsplit")
+        out = torch.empty_like(first)
+        for rep in range(6):
+            P.conv2d_nchw16c(x, pw, stride=1, pad=R // 2, mode=mode, cfg=cfg, out=out)
+            assert torch.equal(out, first), (s, rep)
