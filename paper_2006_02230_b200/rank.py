@@ -340,13 +340,19 @@ _MODEL_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "machines
 class PipelineModel:
     """Per-tile cost of the persistent tile engine, in SM cycles.
 
+    The geometry is the schedule the library itself will run (variants.schedule ->
+    pdl_conv2d_schedule): tile shape, halo mode, resident weights, split-K ranges.
     k-block time = max(tensor pipe, operand feed) + handshake:
       pipe  = mmas_per_kblock * (mma_fixed + mma_per_n * BN)
-      feed  = bytes_per_kblock / l2_bytes_per_cycle   (cluster multicast divides B)
+      feed  = bytes_per_kblock / l2_bytes_per_cycle: A = the 128-row box per tap, or
+              with halo mode the tile's input halo amortised over the R*S taps of a
+              channel group; B = the weight slice (0 when resident; cluster multicast
+              divides it)
       handshake = kblock_fixed + cluster_kb * (cluster - 1)
-    tile time = num_kb * k-block time + tile_fixed;  waves over the CTAs the
-    cluster shape lets the GPU keep resident (4-CTA clusters fit on 132 of the
-    148 SMs); floor at the compulsory HBM bytes.  Constants are fitted on
+    unit time = k-blocks per unit * k-block time + tile_fixed (+ split_fixed when the
+    reduction is split: partial publish and the last unit's reduction); waves of units
+    over the CTAs the cluster shape lets the GPU keep resident (4-CTA clusters fit on
+    132 of the 148 SMs); floor at the compulsory HBM bytes.  Constants are fitted on
     measured B200 sweeps (scripts/fit_ranker.py -> machines/b200_engine.json)."""
     mma_fixed: float = 10.0
     mma_per_n: float = 0.6
@@ -354,6 +360,7 @@ class PipelineModel:
     kblock_fixed: float = 120.0
     cluster_kb: float = 20.0
     tile_fixed: float = 900.0
+    split_fixed: float = 2000.0
     active_ctas: dict = field(default_factory=lambda: {"1": 148, "2": 148, "4": 132})
     launch_us: float = 4.0
     clock_ghz: float = 1.92
@@ -376,22 +383,29 @@ class PipelineModel:
     def terms(self, layer, variant, n_images: int) -> dict:
         from .variants import engine_geometry
         g = engine_geometry(layer, variant, n_images, self.sms)
-        split = variant.mode == "3xtf32"
-        mmas = (3 if split else 1) * (g["ks"] // 8)
-        planes = 2 if split else 1
-        a_bytes = 128 * g["ks"] * 4
-        b_bytes = variant.bn * g["ks"] * 4 * planes / variant.cluster
-        ctas = int(self.active_ctas.get(str(variant.cluster), self.sms))
-        waves = math.ceil(g["tiles"] / ctas)
-        return {"num_kb": g["num_kb"], "mmas": mmas, "feed_bytes": a_bytes + b_bytes,
-                "waves": waves, "bn": variant.bn, "cluster": variant.cluster,
+        three = variant.mode == "3xtf32"
+        ks = g["ks"]
+        mmas = (3 if three else 1) * (ks // 8)
+        planes = 2 if three else 1
+        bn, cl = g["bn"], max(1, g["cluster"])
+        a_bytes = 128 * ks * 4
+        if g.get("halo") and g.get("kind") == 1:
+            taps = layer.R * layer.S
+            halo_px = (g["bw"] + layer.S - 1) * (g["bh"] + layer.R - 1) * g["bni"]
+            a_bytes = halo_px * ks * 4 / taps
+        b_bytes = 0.0 if g.get("resident") else bn * ks * 4 * planes / cl
+        ctas = int(self.active_ctas.get(str(cl), self.sms))
+        split = max(1, g.get("split", 1))
+        waves = math.ceil(g["tiles"] * split / ctas)
+        return {"num_kb": g.get("kb_per", g["num_kb"]), "mmas": mmas, "feed_bytes": a_bytes + b_bytes,
+                "waves": waves, "bn": bn, "cluster": cl, "split": split,
                 "hbm_bytes": layer.bytes(n_images)}
 
     def predict_cycles_per_tile(self, t: dict) -> float:
         pipe = t["mmas"] * (self.mma_fixed + self.mma_per_n * t["bn"])
         feed = t["feed_bytes"] / self.l2_bytes_per_cycle
         kb = max(pipe, feed) + self.kblock_fixed + self.cluster_kb * (t["cluster"] - 1)
-        return t["num_kb"] * kb + self.tile_fixed
+        return t["num_kb"] * kb + self.tile_fixed + (self.split_fixed if t.get("split", 1) > 1 else 0.0)
 
     def predict_seconds(self, layer, variant, n_images: int) -> float:
         t = self.terms(layer, variant, n_images)
@@ -410,7 +424,7 @@ class PipelineModel:
         pipe = per * t["mmas"] * (self.mma_fixed + self.mma_per_n * t["bn"])
         feed = per * t["feed_bytes"] / self.l2_bytes_per_cycle
         hand = per * (self.kblock_fixed + self.cluster_kb * (t["cluster"] - 1)) + \
-            t["waves"] * self.tile_fixed / hz
+            t["waves"] * (self.tile_fixed + (self.split_fixed if t["split"] > 1 else 0.0)) / hz
         return VariantStats(variant.vid, pipe, feed, hand, t["hbm_bytes"] / (self.hbm_gbs * 1e9))
 
 
@@ -429,6 +443,9 @@ def rank_by_model(layer, variants, n_images: int, model: PipelineModel = None) -
 _RANKER_FILE = os.path.join(os.path.dirname(_MODEL_FILE), "b200_ranker.npz")
 
 
+DNN_SHORTLIST = 16
+
+
 def choose_variant(layer, n_images: int, mode: str = "3xtf32", method: str = "dnn",
                    model: PipelineModel = None, judge: RankerModel = None):
     """Pick the schedule for a conv layer among its legal tile variants.
@@ -436,9 +453,12 @@ def choose_variant(layer, n_images: int, mode: str = "3xtf32", method: str = "dn
     method "dnn": tournament of the trained pairwise judge over the pipeline
     model's per-resource terms (machines/b200_ranker.npz), ties broken by the
     model's predicted time; "model": the fitted pipeline model alone; "cost":
-    Eq. 1 over the tile working sets."""
+    Eq. 1 over the tile working sets.  The menu is the full variant space of the
+    shape at this batch (tile sizes, tile order, halo, segment tiles, split-K when
+    the tiles leave SMs idle); the judge's tournament runs over the model's top
+    `DNN_SHORTLIST` (its pairwise cost is quadratic)."""
     from .variants import VariantConfig, generate_variants
-    vs = generate_variants(layer, VariantConfig(modes=(mode,)))
+    vs = generate_variants(layer, VariantConfig(modes=(mode,)), n_images=n_images)
     if not vs:
         raise RankError(f"no legal variant for {layer}")
     if len(vs) == 1:
@@ -455,7 +475,8 @@ def choose_variant(layer, n_images: int, mode: str = "3xtf32", method: str = "dn
             if not os.path.exists(_RANKER_FILE):
                 raise RankError(f"no trained judge at {_RANKER_FILE}; run scripts/fit_ranker.py")
             judge = RankerModel.load(_RANKER_FILE)
-        t = tournament_rank(judge, [pm.term_stats(layer, v, n_images) for v in vs],
+        short = set(by_model.order[:DNN_SHORTLIST])
+        t = tournament_rank(judge, [pm.term_stats(layer, v, n_images) for v in vs if v.vid in short],
                             both_directions=True)
         wins = dict(t.scores)
         pos = {v: i for i, v in enumerate(by_model.order)}

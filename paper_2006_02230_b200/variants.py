@@ -1,35 +1,51 @@
 """Schedule variants of the B200 tile engine (SPEC `variants` module,
 SPEC.md:468-529, re-targeted).
 
-On the CPU a variant is a tiled / interchanged loop nest emitted as C.  On the
-B200 the loop nest is fixed (the persistent tile engine), and what varies is
-the tile configuration a `pdl_tile_cfg` carries:
+On the CPU a variant is a tiled / interchanged loop nest with one loop marked
+parallel, emitted as C.  On the B200 the engine executes the Fig. 9 / Fig. 1 nest
+as a persistent implicit GEMM, and the same three transformation families become
+the fields of a `pdl_tile_cfg`:
 
-  bn       output channels (conv K / GEMM N) per CTA tile: 64 | 128 | 256 (TF32 only:
-           one accumulation segment per tile, streaming epilogue)
-  bk       reduction elements per pipeline stage: 16 * cg, cg in {1, 2, 4}
-  cluster  CTAs sharing (multicasting) each weight tile: 1 | 2 | 4
-  mode     "3xtf32" | "tf32"
+  tiling        bn      output channels (conv K / GEMM N) per CTA tile: 64 | 128 |
+                        256 (TF32 only: one accumulation segment, streaming epilogue)
+                bk      reduction elements per k-block: 16 * cg, cg in {1, 2, 4}
+                seg     output-pixel tile shape: box tiles ("off") or segment tiles
+                        spanning images ("on"; small 1x1 maps), "auto" = library rule
+                halo    stride-1 spatial convs: the tile's input halo loaded once per
+                        channel group ("on") or one A box per tap ("off")
+  interchange   order   tile loop order: output-channel tiles fastest ("n": CTAs
+                        running together share activation rows) or output-pixel tiles
+                        fastest ("m": they share a weight slice)
+  parallel loop split   the reduction loop split across CTAs (split-K): 1 = the tile
+                        loops alone are parallel; k > 1 = the reduction loop too, in k
+                        ranges; 0 = library planner (only with sub-wave tile counts)
+                cluster CTAs sharing (multicasting) each weight tile: 1 | 2 | 4
 
-`generate_variants` enumerates the legal ones deterministically (ids sorted,
-deduplicated), `legality_check` runs a variant against the default schedule on
-the GPU (interpreter-equivalence in the SPEC's sense, at the mode's tolerance:
-variants with the same bk and segmenting reduce every element in the same order
-and agree bitwise; a different bk re-associates the channel/tap sum inside a
-256-element accumulation segment, and 256-column tiles sum the whole reduction in
-one segment), `emit_launch` is the B200 analogue of
-`emit_c`: the launch configuration (a dict accepted as `cfg=` by the ops).
-`engine_geometry` restates the host's tiling rules (csrc/pdl_capi.cu) so the
-analytical ranker can reason about a variant without launching it.
+`generate_variants(nest, cfg, binding)` takes the `.pdl` LoopNest (the conv /
+GEMM nest is recognised by the executor's matcher) or an already
+recognised layer shape, enumerates the menus, and keeps one variant per distinct
+EFFECTIVE schedule: every candidate is run through the library's own planner
+(`pdl_conv2d_schedule` / `pdl_gemm_schedule`, host-only) so that a request the
+engine would silently override (halo on a 1x1 layer, a split on a full wave,
+segment tiles on an odd-width map) does not appear as a separate variant.  Ids are
+deterministic (sorted); the first id per schedule wins.  `legality_check` runs a
+variant against the default schedule on the GPU (interpreter equivalence at the
+mode tolerance); `emit_launch` is the B200 analogue of `emit_c`: the launch
+configuration (a dict accepted as `cfg=` by the ops); `emit_nest` writes the
+variant's tiled loop nest as `.pdl` text (provenance, parseable).
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 # kernel instances compiled into libpdl.so (csrc/pdl_capi.cu dispatch_bn)
 _CONV_INSTANCES = {(64, 1), (64, 2), (64, 4), (128, 1), (128, 2)}
 _SMEM_BUDGET = 216 * 1024
 _SEG_ELEMS = 256
+_SMS = 148
+
+# include/pdl.h raster bits
+RASTER_M_FASTEST, RASTER_BOX_TILES, RASTER_SEG_TILES, RASTER_NO_HALO, RASTER_HALO_CG4 = 1, 2, 4, 16, 64
 
 
 @dataclass(frozen=True, order=True)
@@ -39,10 +55,40 @@ class TileVariant:
     bk: int
     cluster: int
     mode: str = "3xtf32"
+    order: str = "n"      # "n": output-channel tiles fastest, "m": output-pixel tiles fastest
+    halo: str = "auto"    # "on" | "off" | "auto"
+    seg: str = "auto"     # "on" | "off" | "auto"
+    split: int = 0        # 0: library planner, 1: no split, k: k reduction ranges
 
     @property
     def cg(self) -> int:
         return self.bk // 16
+
+    def provenance(self) -> dict:
+        return {"bn": self.bn, "bk": self.bk, "cluster": self.cluster, "mode": self.mode,
+                "order": self.order, "halo": self.halo, "seg": self.seg, "split": self.split}
+
+
+def make_variant(bn: int, bk: int, cluster: int, mode: str = "3xtf32", order: str = "n",
+                 halo: str = "auto", seg: str = "auto", split: int = 0) -> TileVariant:
+    """Variant with its canonical id (defaults leave no suffix, so the ids of the
+    round-1 bn x bk x cluster menu are unchanged)."""
+    vid = f"bn{bn}_bk{bk}_c{cluster}_{mode}"
+    if order == "m":
+        vid += "_om"
+    if halo != "auto":
+        vid += "_h1" if halo == "on" else "_h0"
+    if seg != "auto":
+        vid += "_s1" if seg == "on" else "_s0"
+    if split:
+        vid += f"_k{split}"
+    return TileVariant(vid, bn, bk, cluster, mode, order, halo, seg, split)
+
+
+def variant_from_record(vid: str, rec: dict, mode: str) -> TileVariant:
+    """Rebuild a variant from a sweep record (scripts/sweep_variants.py)."""
+    return TileVariant(vid, rec["bn"], rec["bk"], rec["cluster"], mode, rec.get("order", "n"),
+                       rec.get("halo", "auto"), rec.get("seg", "auto"), rec.get("split", 0))
 
 
 @dataclass
@@ -51,7 +97,11 @@ class VariantConfig:
     cg_menu: tuple = (1, 2, 4)
     cluster_menu: tuple = (1, 2, 4)
     modes: tuple = ("3xtf32",)
-    cap: int = 64
+    order_menu: tuple = ("n", "m")
+    halo_menu: tuple = ("auto", "on", "off")
+    seg_menu: tuple = ("auto", "on", "off")
+    split_menu: tuple = (0, 1, 2, 3, 4, 6, 8)   # used only when the tiles leave SMs idle
+    cap: int = 256
 
 
 def _is_gemm(layer) -> bool:
@@ -62,19 +112,25 @@ def _is_stem(layer) -> bool:
     return not _is_gemm(layer) and layer.C <= 4 and layer.S <= 8 and layer.R <= 7
 
 
+def _mode_flags(mode: str) -> int:
+    from ._lib import MODES
+    return MODES[mode]
+
+
 def legal(layer, v: TileVariant) -> bool:
     """Static legality: a compiled instance exists, channel grouping matches
     the packed weight rows, the stage fits shared memory / TMEM."""
     if _is_gemm(layer):
         # GEMM instances: bn in {64, 128}, bk = 32, cluster in {1, 2, 4}
         return v.bk == 32 and v.bn in (64, 128) and v.cluster in (1, 2, 4) and \
-            not (v.bn > 64 and layer.N <= 64)
+            not (v.bn > 64 and layer.N <= 64) and v.halo == "auto" and v.seg == "auto"
     if _is_stem(layer):
-        return v.bn == 64 and v.cluster == 1 and v.bk == 32
+        return v.bn == 64 and v.cluster == 1 and v.bk == 32 and v.order == "n" and \
+            v.halo == "auto" and v.seg == "auto" and v.split in (0, 1)
     ct = (layer.C + 15) // 16
     if v.bn == 256:
-        # TF32 instance only, whole 256-column slices, no cluster (conv_default_cfg)
-        if not (v.mode == "tf32" and v.cg == 2 and v.cluster == 1 and layer.K % 256 == 0):
+        # TF32 instance only, whole 256-column slices, no cluster / split (conv_default_cfg)
+        if not (v.mode == "tf32" and v.cg == 2 and v.cluster == 1 and layer.K % 256 == 0 and v.split in (0, 1)):
             return False
     elif (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
         return False
@@ -86,6 +142,8 @@ def legal(layer, v: TileVariant) -> bool:
         return False
     if v.bn > 64 and layer.K <= 64:
         return False
+    if v.cluster > 1 and (v.order == "m" or v.halo == "on"):
+        return False                        # tile order / halo need cluster 1
     g = stage_sizes(v)
     return g["stages"] >= 2 and (v.mode != "3xtf32" or g["tslots"] >= 2)
 
@@ -102,8 +160,46 @@ def stage_sizes(v: TileVariant) -> dict:
     return {"stage_bytes": stage, "stages": stages, "ks": ks, "tslots": tslots}
 
 
+def emit_launch(v: TileVariant) -> dict:
+    """Launch configuration for the ops (`cfg=`), the B200 analogue of emit_c:
+    the fields of `pdl_tile_cfg` (include/pdl.h)."""
+    raster = 0
+    if v.order == "m":
+        raster |= RASTER_M_FASTEST
+    if v.halo == "off":
+        raster |= RASTER_NO_HALO
+    elif v.halo == "on" and v.cg == 4 and v.mode == "3xtf32":
+        raster |= RASTER_HALO_CG4
+    if v.seg == "off":
+        raster |= RASTER_BOX_TILES
+    elif v.seg == "on":
+        raster |= RASTER_SEG_TILES
+    cfg = {"bm": 128, "bn": v.bn, "bk": v.bk, "cluster_m": v.cluster}
+    if raster:
+        cfg["raster"] = raster
+    if v.split:
+        cfg["split_k"] = v.split
+    return cfg
+
+
+def schedule(layer, v: TileVariant, n_images: int) -> dict:
+    """The schedule libpdl will actually run for this variant (pdl_conv2d_schedule /
+    pdl_gemm_schedule; host-only, no GPU needed)."""
+    from ._lib import conv_schedule, gemm_schedule
+    if _is_gemm(layer):
+        return gemm_schedule(layer.M, layer.N, layer.K, _mode_flags(v.mode), emit_launch(v))
+    return conv_schedule(n_images, layer.C, layer.K, layer.H, layer.W, layer.R, layer.S, layer.stride,
+                         layer.pad, _mode_flags(v.mode), emit_launch(v))
+
+
+def _signature(sched: dict, v: TileVariant) -> tuple:
+    keys = ("kind", "bn", "bk", "cluster", "tile_w", "tile_h", "tile_images", "seg_rows", "m_tiles",
+            "n_tiles", "split", "kb_per", "halo", "resident", "pair", "order")
+    return (v.mode,) + tuple(sched[k] for k in keys)
+
+
 def stem_tile(layer) -> tuple:
-    """BW x BH output-pixel tile of the narrow-channel stem (conv_fwd_stem in
+    """BW x BH output-pixel tile of the narrow-channel stem (stem_tile in
     csrc/pdl_capi.cu): its input halo is one TMA box / pipeline stage."""
     P, Q, s, R, S = layer.P, layer.Q, layer.stride, layer.R, layer.S
     best, pick = float("inf"), None
@@ -119,49 +215,83 @@ def stem_tile(layer) -> tuple:
     return pick
 
 
-def engine_geometry(layer, v: TileVariant, n_images: int, sms: int = 148) -> dict:
-    """Tile geometry the host code picks (conv_geom in csrc/pdl_capi.cu)."""
+def engine_geometry(layer, v: TileVariant, n_images: int, sms: int = _SMS) -> dict:
+    """Tile geometry of the schedule the library runs (from its own planner)."""
     g = stage_sizes(v)
-    if _is_gemm(layer):
-        m_tiles, n_tiles = -(-layer.M // 128), -(-layer.N // v.bn)
-        g.update(flat=True, bw=128, bh=1, bni=1, rows_valid=min(layer.M, 128), m_eff=1.0,
-                 m_tiles=m_tiles, n_tiles=n_tiles, tiles=m_tiles * n_tiles,
-                 num_kb=-(-layer.K // 32), seg_kb=max(1, _SEG_ELEMS // 32),
-                 tiles_concurrent=sms, tile_rows_in=1)
-        return g
-    P, Q = layer.P, layer.Q
-    flat = layer.R == 1 and layer.S == 1 and layer.stride == 1 and layer.pad == 0
-    Pg, Qg = (1, P * Q) if flat else (P, Q)
-    if _is_stem(layer):
-        bw, bh = stem_tile(layer)
-        bni = 1
-    else:
-        bw = min(Qg, 128)
-        bh = min(Pg, 128 // bw)
-        bni = max(1, min(n_images, 128 // (bw * bh))) if bh == Pg else 1
-    tiles_w, tiles_h = -(-Qg // bw), -(-Pg // bh)
-    m_tiles = tiles_w * tiles_h * -(-n_images // bni)
-    n_tiles = -(-layer.K // v.bn)
-    rows = bw * bh * bni
-    num_kb = layer.R if _is_stem(layer) else ((layer.C_alloc // 16) // v.cg) * layer.R * layer.S
-    g.update(flat=flat, bw=bw, bh=bh, bni=bni, rows_valid=rows, m_eff=rows / 128.0,
-             m_tiles=m_tiles, n_tiles=n_tiles, tiles=m_tiles * n_tiles, num_kb=num_kb,
-             seg_kb=num_kb if v.bn > 128 else max(1, _SEG_ELEMS // g["ks"]), tiles_concurrent=sms,
-             tile_rows_in=(bh - 1) * layer.stride + layer.R)
+    s = schedule(layer, v, n_images)
+    rows = s["tile_w"] * s["tile_h"] * (1 if s["seg_rows"] else s["tile_images"])
+    g.update(s)
+    g.update(bw=s["tile_w"], bh=s["tile_h"], bni=s["tile_images"], rows_valid=min(rows, 128),
+             m_eff=min(rows, 128) / 128.0, tiles=s["m_tiles"] * s["n_tiles"],
+             units=s["m_tiles"] * s["n_tiles"] * max(1, s["split"]),
+             seg_kb=s["num_kb"] if s["bn"] > 128 else max(1, _SEG_ELEMS // max(g["ks"], 1)),
+             tiles_concurrent=sms, ks=(s["bk"] if not _is_gemm(layer) else 32),
+             tile_rows_in=1 if _is_gemm(layer) else (s["tile_h"] - 1) * layer.stride + layer.R,
+             flat=bool(s["flat"]))
     return g
 
 
-def generate_variants(layer, cfg: VariantConfig = VariantConfig()) -> list:
-    """All legal tile configurations of a conv layer, deterministic order."""
-    out = {}
+def _shape_of(nest, binding):
+    """(layer shape, images) of a conv / GEMM LoopNest, via the executor's matcher."""
+    from .executor import ConvPlan, GemmPlan, plan_program
+    from .workloads import ConvShape, GemmShape
+    plans = plan_program([nest], binding)
+    heavy = [p for p in plans if isinstance(p, (ConvPlan, GemmPlan))]
+    if len(heavy) != 1:
+        raise ValueError("generate_variants: the nest is not one conv / GEMM")
+    p = heavy[0]
+    if isinstance(p, GemmPlan):
+        return GemmShape(p.M, p.N, p.K), 1
+    # the nest's input is pre-padded (Fig. 9); the B200 call takes it unpadded with pad 0
+    return ConvShape(p.CT * 16, p.KT * 16, p.Hp, p.Wp, p.R, p.S, p.stride, 0), p.N
+
+
+def generate_variants(nest_or_layer, cfg: VariantConfig = VariantConfig(), binding=None,
+                      n_images: int | None = None) -> list:
+    """All legal, distinct schedules of a conv / GEMM, deterministic id order.
+
+    `nest_or_layer`: a LoopNest (with `binding`) -- SPEC.md:483's signature -- or a
+    layer shape (workloads.ConvLayer / ConvShape / GemmShape).  `n_images` (taken
+    from the nest when given one) decides whether split-K candidates exist: they do
+    only when the unsplit tiles leave SMs idle."""
+    from .loopnest import LoopNest
+    if isinstance(nest_or_layer, LoopNest):
+        if binding is None:
+            raise ValueError("generate_variants(nest): a parameter binding is required")
+        layer, n = _shape_of(nest_or_layer, binding)
+        n_images = n if n_images is None else n_images
+    else:
+        layer = nest_or_layer
+    n = 256 if n_images is None else n_images
+    gemm, stem = _is_gemm(layer), _is_stem(layer)
+    seen: dict = {}
     for mode in cfg.modes:
         for bn in cfg.bn_menu:
-            for cg in ((2,) if _is_gemm(layer) else cfg.cg_menu):
+            for cg in ((2,) if gemm else cfg.cg_menu):
                 for cl in cfg.cluster_menu:
-                    v = TileVariant(f"bn{bn}_bk{16 * cg}_c{cl}_{mode}", bn, 16 * cg, cl, mode)
-                    if legal(layer, v):
-                        out[v.vid] = v
-    vs = [out[k] for k in sorted(out)]
+                    v0 = make_variant(bn, 16 * cg, cl, mode)
+                    if not legal(layer, v0):
+                        continue
+                    try:
+                        s0 = schedule(layer, v0, n)
+                    except Exception:  # noqa: BLE001 -- the planner refused the combination
+                        continue
+                    sub_wave = s0["m_tiles"] * s0["n_tiles"] < _SMS and n_images is not None
+                    splits = cfg.split_menu if sub_wave else (0,)
+                    for order in (cfg.order_menu if cl == 1 else ("n",)):
+                        for halo in (("auto",) if gemm or stem else cfg.halo_menu):
+                            for seg in (("auto",) if gemm or stem else cfg.seg_menu):
+                                for sp in splits:
+                                    v = make_variant(bn, 16 * cg, cl, mode, order, halo, seg, sp)
+                                    if not legal(layer, v):
+                                        continue
+                                    try:
+                                        sig = _signature(schedule(layer, v, n), v)
+                                    except Exception:  # noqa: BLE001
+                                        continue
+                                    if sig not in seen or v.vid < seen[sig].vid:
+                                        seen[sig] = v
+    vs = sorted(seen.values(), key=lambda v: v.vid)
     if not vs:
         import warnings
         warnings.warn(f"no legal variant for {layer.name()}; using the default only")
@@ -171,10 +301,41 @@ def generate_variants(layer, cfg: VariantConfig = VariantConfig()) -> list:
     return vs[:cfg.cap]
 
 
-def emit_launch(v: TileVariant) -> dict:
-    """Launch configuration for the ops (`cfg=`), the B200 analogue of emit_c:
-    the fields of `pdl_tile_cfg` (include/pdl.h)."""
-    return {"bm": 128, "bn": v.bn, "bk": v.bk, "cluster_m": v.cluster}
+def emit_nest(layer, v: TileVariant, n_images: int = 1) -> str:
+    """The variant as a transformed loop nest (SPEC `Variant.nest`), `.pdl` text.
+
+    GEMM: the Fig. 1 nest tiled the way the engine runs it -- the two tile loops in
+    the variant's order (the outer one `parallel`), the reduction cut into the
+    split-K ranges and k-blocks, and the 128 x bn x 32 microkernel band innermost.
+    It parses with loopnest.parse and is interpreter-equivalent to Fig. 1 (the
+    reduction is only re-associated).  Conv: a one-line provenance comment of the
+    effective schedule (its tile shapes -- segment tiles spanning images, halo
+    reuse -- are not loop tilings of the Fig. 9 nest)."""
+    s = schedule(layer, v, n_images)
+    if not _is_gemm(layer):
+        tiles = "pixel tiles" if not s["seg_rows"] else f"segment tiles of {s['seg_rows']} rows"
+        return (f"// {layer.name()} x{n_images} {v.vid}: {s['m_tiles']} {tiles} "
+                f"({s['tile_w']}x{s['tile_h']}x{s['tile_images']}) x {s['n_tiles']} channel tiles of "
+                f"{s['bn']}; {s['num_kb']} k-blocks of {s['bk']} in {s['split']} range(s) of "
+                f"{s['kb_per']}; halo {'on' if s['halo'] else 'off'}; resident weights "
+                f"{'on' if s['resident'] else 'off'}; "
+                f"{'pixel' if s['order'] else 'channel'}-tiles fastest\n")
+    bn, kr = s["bn"], s["kb_per"] * 32
+    loops = [("it", "M", 128), ("jt", "N", bn)]
+    if s["order"] == 1:
+        loops.reverse()
+    (o1, e1, t1), (o2, e2, t2) = loops
+    lines = ["param M, N, K;", "array C[M][N];", "array A[M][K];", "array B[K][N];",
+             f"gemm: parallel for ({o1} = 0; {o1} < {e1}; {o1} += {t1}) {{",
+             f"  for ({o2} = 0; {o2} < {e2}; {o2} += {t2}) {{",
+             f"    for (kr = 0; kr < K; kr += {kr}) {{",
+             "      for (kt = kr; kt < min(kr + %d, K); kt += 32) {" % kr,
+             "        for (i = it; i < min(it + 128, M); i++) {",
+             f"          for (j = jt; j < min(jt + {bn}, N); j++) {{",
+             "            for (k = kt; k < min(kt + 32, K); k++) {",
+             "              S: C[i][j] += A[i][k] * B[k][j];",
+             "            }", "          }", "        }", "      }", "    }", "  }", "}"]
+    return "\n".join(lines) + "\n"
 
 
 MODE_TOLERANCE = {"3xtf32": 1e-5, "tf32": 1e-2}
@@ -200,3 +361,8 @@ def legality_check(layer, v: TileVariant, n_images: int = 2, seed: int = 0,
     rel = float((got - ref).abs().max()) / scale
     ok = bool(np.isfinite(got.cpu().numpy()).all()) and rel <= MODE_TOLERANCE[v.mode]
     return (ok, {"bitwise": bitwise, "max_rel": rel}) if return_detail else ok
+
+
+__all__ = ["TileVariant", "VariantConfig", "make_variant", "variant_from_record", "legal", "stage_sizes",
+           "emit_launch", "schedule", "engine_geometry", "generate_variants", "emit_nest",
+           "legality_check", "MODE_TOLERANCE", "stem_tile"]

@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--modes", default="3xtf32,tf32")
     ap.add_argument("--layers", default="")
+    ap.add_argument("--cap", type=int, default=256, help="variants per layer and mode")
     args = ap.parse_args()
     torch.manual_seed(0)
     m = default_machine()
@@ -77,7 +78,7 @@ def main():
             PW = ops.prepack_weights(Wt, mode, channels=L.C)
             ref = ops.conv2d_nchw16c(X2, PW, Bt, stride=L.stride, pad=L.pad, relu=True,
                                      mode=mode, channels=L.C)
-            vs = variants.generate_variants(L, variants.VariantConfig(modes=(mode,)))
+            vs = variants.generate_variants(L, variants.VariantConfig(modes=(mode,), cap=args.cap), n_images=n)
             rows = {}
             for v in vs:
                 cfg = variants.emit_launch(v)
@@ -88,14 +89,15 @@ def main():
                 legal = rel <= variants.MODE_TOLERANCE[mode]
                 med, best = time_variant(L, X, PW, Bt, cfg, mode, args.reps, flush)
                 st = rank.stats_for_variant(L, v, n, m)
-                rows[v.vid] = {"bn": v.bn, "bk": v.bk, "cluster": v.cluster, "legal": legal, "bitwise": bitwise, "max_rel": rel,
+                rows[v.vid] = {**v.provenance(), "legal": legal, "bitwise": bitwise, "max_rel": rel,
+                               "schedule": variants.schedule(L, v, n),
                                "ms": med, "ms_min": best,
                                "tflops": L.flops(n) / (med * 1e-3) / 1e12,
                                "model_ms": pm.predict_seconds(L, v, n) * 1e3,
                                "cost": float(rank.cost_of_stats(st, m)),
                                "stats": [st.ws_l1, st.ws_l2, st.ws_l3, st.ws_mem]}
             med, best = time_variant(L, X, PW, Bt, None, mode, args.reps, flush)
-            doc["layers"].append({"layer": L.name(), "idx": L.idx, "mode": mode,
+            doc["layers"].append({"layer": L.name(), "idx": L.idx, "mode": mode, "batch": n,
                                   "C": L.C, "K": L.K, "H": L.H, "R": L.R, "stride": L.stride,
                                   "flops": L.flops(n), "default_ms": med, "variants": rows})
             order = sorted(rows, key=lambda k: rows[k]["ms"])
