@@ -265,6 +265,54 @@ def _par_footprint(tr, by_label, p, sample_outer) -> int:
     return best
 
 
+# ----------------------------------------------------------------------------- engine nest
+def engine_gemm_nest(bm: int, bn: int, bk: int) -> str:
+    """The tile engine's GEMM schedule as a `.pdl` nest (variants.emit_nest without
+    split-K, tile sizes free so it can be enumerated at desk-size bindings): tile
+    loops it, jt, kt, then the bm x bn x bk band."""
+    return f"""param M, N, K;
+array C[M][N];
+array A[M][K];
+array B[K][N];
+gemm: parallel for (it = 0; it < M; it += {bm}) {{
+  for (jt = 0; jt < N; jt += {bn}) {{
+    for (kt = 0; kt < K; kt += {bk}) {{
+      for (i = it; i < min(it + {bm}, M); i++) {{
+        for (j = jt; j < min(jt + {bn}, N); j++) {{
+          for (k = kt; k < min(kt + {bk}, K); k++) {{
+            S: C[i][j] += A[i][k] * B[k][j];
+          }}
+        }}
+      }}
+    }}
+  }}
+}}
+"""
+
+
+def engine_gemm_working_sets(bm: int, bn: int, bk: int, M: int, N: int, K: int) -> WorkingSetReport:
+    """Alg. 1's working sets of engine_gemm_nest in closed form (elements), valid when
+    the tiles divide the extents and K >= 2 bk, N >= 2 bn:
+      C (accumulator, RAR/RAW/WAR/WAW of C[i][j] across the k-blocks of its tile)
+          WS_min = 5 (the next k step), WS_max = bm bn + (bm + bn)(K - bk) + 2 bk
+          -- one TMEM accumulator + the tile's A and B panels (tile_working_sets'
+          tmem.acc / 2 + l2.Apanel + l2.Bpanel) less the last k-block's panels;
+      A (A[i][k] reused across j and the N-tiles) WS_min = 2 bk + 3,
+          WS_max = bm K + (N - bn)(K + bm) + bk (bn - 1) + 1 + bn;
+      B (B[k][j] reused across the parallel it loop) WS_par = MK + KN + MN.
+    tests/test_rank.py checks these against the enumerated Alg. 1 (working_sets,
+    itself pinned to the reference) at desk-size bindings."""
+    c_max = bm * bn + (bm + bn) * (K - bk) + 2 * bk
+    a_max = bm * K + (N - bn) * (K + bm) + bk * (bn - 1) + 1 + bn
+    e = [WorkingSetEntry("S:r0->S:r0", "RAR", "A", "min", 2 * bk + 3),
+         WorkingSetEntry("S:r0->S:r0", "RAR", "A", "max", a_max),
+         WorkingSetEntry("S:r1->S:r1", "RAR", "B", "par", M * K + K * N + M * N)]
+    for dep, kind in (("S:r2->S:r2", "RAR"), ("S:r2->S:w0", "WAR"), ("S:w0->S:r2", "RAW"),
+                      ("S:w0->S:w0", "WAW")):
+        e += [WorkingSetEntry(dep, kind, "C", "min", 5), WorkingSetEntry(dep, kind, "C", "max", c_max)]
+    return WorkingSetReport("gemm", (("K", K), ("M", M), ("N", N)), tuple(e))
+
+
 # ----------------------------------------------------------------------------- tile form
 def tile_working_sets(layer, variant, n_images: int, sms: int = 148) -> WorkingSetReport:
     """Closed-form working sets of one tile-engine schedule on one SM.

@@ -316,3 +316,33 @@ def test_dependences_and_domains_match_reference(case):
         else:
             assert [lo[v] for v in dom["vars"]] == dom["lexmin"]
             assert [hi[v] for v in dom["vars"]] == dom["lexmax"]
+
+
+# ----------------------------------------------------------------------------- tile form vs Alg. 1
+@pytest.mark.parametrize("tiles", [(2, 2, 2, 4, 4, 4), (2, 3, 2, 4, 6, 6), (3, 2, 2, 6, 4, 6),
+                                   (2, 2, 3, 4, 4, 9), (4, 2, 2, 8, 4, 4), (1, 4, 2, 2, 8, 6)])
+def test_engine_nest_working_sets_closed_form_vs_alg1(tiles):
+    """The tile engine's schedule written as a loop nest, enumerated by Alg. 1
+    (wset.working_sets, pinned to the reference) at desk-size bindings, equals the
+    closed forms the B200 tile working sets are built from."""
+    from paper_2006_02230_b200 import wset as WS
+    bm, bn, bk, M, N, K = tiles
+    enum = WS.working_sets(parse(WS.engine_gemm_nest(bm, bn, bk)), dict(M=M, N=N, K=K))
+    closed = WS.engine_gemm_working_sets(bm, bn, bk, M, N, K)
+    key = lambda e: (e.dep_id, e.variant)  # noqa: E731
+    assert sorted((key(e), e.elements) for e in enum.entries) == \
+        sorted((key(e), e.elements) for e in closed.entries)
+
+
+def test_tile_working_sets_leading_terms_match_closed_form():
+    """At BASELINE sizes the tile form's accumulator + panel entries are the leading
+    terms of Alg. 1's accumulator working set of the engine nest."""
+    from paper_2006_02230_b200 import wset as WS
+    for (m, n, k) in [(1024, 1024, 1024), (4096, 4096, 4096), (3136, 64, 576)]:
+        g = workloads.GemmShape(m, n, k)
+        for v in V.generate_variants(g):
+            rep = {e.dep_id: e.elements for e in WS.tile_working_sets(g, v, 1).entries}
+            closed = WS.engine_gemm_working_sets(128, v.bn, 32, m, n, k)
+            c_max = next(e.elements for e in closed.entries if e.array == "C" and e.variant == "max")
+            lead = rep["tmem.acc"] // 2 + rep["l2.Apanel"] + rep["l2.Bpanel"]
+            assert c_max == lead - (128 + v.bn) * 32 + 2 * 32, (m, n, k, v.vid)
