@@ -101,7 +101,7 @@ def cmd_rank(a) -> int:
     from .machine import default_machine, load_machine
     shape, n, _ = _workload(_load(a.file), a.binding)
     m = load_machine(a.machine) if a.machine else default_machine()
-    vs = variants.generate_variants(shape, variants.VariantConfig(modes=(a.mode,)))
+    vs = variants.generate_variants(shape, variants.VariantConfig(modes=(a.mode,)), n_images=n)
     if not vs:
         raise ValueError("no legal variant")
     k = a.top_k
@@ -139,8 +139,9 @@ def cmd_rank(a) -> int:
 
 def cmd_emit(a) -> int:
     from . import variants
-    shape, _, _ = _workload(_load(a.file), a.binding)
-    vs = {v.vid: v for v in variants.generate_variants(shape, variants.VariantConfig(modes=(a.mode,)))}
+    shape, n, _ = _workload(_load(a.file), a.binding)
+    vs = {v.vid: v for v in variants.generate_variants(shape, variants.VariantConfig(modes=(a.mode,)),
+                                                      n_images=n)}
     if a.variant not in vs:
         raise _Usage(f"unknown variant {a.variant!r}; legal: {', '.join(sorted(vs))}")
     print(_dump({"version": REPORT_VERSION, "workload": shape.name(), "variant": a.variant,
