@@ -507,6 +507,12 @@ def run_suite(args, rank, world, local):
     # ---- e2e through the public API with host buffers
     if not args.no_e2e:
         out["e2e"] = run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream)
+        # the same step with the stem's x in the compact [N][H][W][4] layout (PDL_X_NCHW4C):
+        # reported beside the nChw16c headline, never instead of it
+        out["e2e_compact_stem"] = run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops,
+                                                stream, compact_stem=True)
+    if rank == 0 and world == 1 and not args.no_extras:
+        out["stem_compact"] = run_stem_compact(args, bufs, P, W, torch, stream, peaks, per_layer)
 
     # ---- unfused GPU baseline comparison (optional)
     if args.unfused:
@@ -547,14 +553,22 @@ def run_suite(args, rank, world, local):
     return out
 
 
-def run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream):
+def compact_x(layer, x):
+    """The narrow-channel layer's x as [N][H][W][4] (its real channels + zero padding)."""
+    return x[:, 0, :, :, :4].contiguous()
+
+
+def run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream, compact_stem=False):
     """Same metric through the public API with pinned HOST buffers: each step
     copies every layer's x host->device, runs the fused conv, and copies y back.
-    Timed over all --steps steps."""
-    hx = [torch.empty(x.shape, dtype=torch.float32, pin_memory=True) for (_, x, *_r) in bufs]
+    Timed over all --steps steps.  compact_stem: layers with C <= 4 (the stem) take
+    their host x as [N][H][W][4] instead of nChw16c's 64-byte pixels."""
+    srcs = [compact_x(layer, x) if (compact_stem and layer.C <= 4) else x for (layer, x, *_r) in bufs]
+    hx = [torch.empty(x.shape, dtype=torch.float32, pin_memory=True) for x in srcs]
     hy = [torch.empty(y.shape, dtype=torch.float32, pin_memory=True) for (*_r, y) in bufs]
-    for h, (_, x, *_r) in zip(hx, bufs):
+    for h, x in zip(hx, srcs):
         h.copy_(x)
+    del srcs
     h2d = sum(h.numel() * 4 for h in hx)
     d2h = sum(h.numel() * 4 for h in hy)
 
@@ -583,7 +597,40 @@ def run_suite_e2e(args, bufs, P, torch, dev, world, dist, total_flops, stream):
             "ms_per_step": round(ms / steps, 3),
             "path": "paper_2006_02230_b200.conv2d_nchw16c_host -> libpdl.so pdl_conv2d_fwd_host "
                     "(pinned host x/y; image chunks pipelined: H2D, fused conv and D2H on three "
-                    "streams), every copy inside the timed region"}
+                    "streams), every copy inside the timed region"
+                    + ("; stem x as [N][H][W][4] (PDL_X_NCHW4C)" if compact_stem else "")}
+
+
+def run_stem_compact(args, bufs, P, W, torch, stream, peaks, per_layer):
+    """The stem with its input in the compact [N][H][W][4] layout (PDL_X_NCHW4C) beside
+    the nChw16c call: back-to-back launches of each, alternating, on the suite's stem
+    buffers (x + y = 1.0 / 1.6 GB per launch >> L2)."""
+    i0 = next((i for i, b in enumerate(bufs) if b[0].C <= 4), None)
+    if i0 is None:
+        return {"skipped": "no narrow-channel layer"}
+    layer, x, w, b, pw, y = bufs[i0]
+    n = x.shape[0]
+    x4 = compact_x(layer, x)
+    mpeak, label = mode_peak(peaks, args.mode)
+
+    def call(xin):
+        return lambda: P.conv2d_nchw16c(xin, pw, b, stride=layer.stride, pad=layer.pad, relu=True,
+                                        mode=args.mode, out=y, channels=layer.C)
+    _, per = time_calls(torch, [call(x), call(x4)], 1, stream, graph=False, per_call=max(5, args.steps))
+    y16 = y.clone()
+    call(x4)()
+    same = bool(torch.equal(y, y16))
+    f = layer.flops(n)
+    hbm = peaks["hbm_gbs"] * 1e9
+    res = {"layer": layer.name(), "bitwise_equal_to_nchw16c": same, "roofline_peak_source": label}
+    for key, ms, stored in (("nchw16c", per[0], n * layer.H * layer.W * 64),
+                            ("nchw4c", per[1], n * layer.H * layer.W * 16)):
+        res[key] = {"ms": round(ms, 4), "gflops": round(f / ms / 1e6, 1),
+                    "tensor_frac": round(f / (ms / 1e3) / mpeak, 3),
+                    "x_bytes_stored": stored,
+                    "hbm_floor_ms": round((stored + n * layer.K * layer.P * layer.Q * 4) / hbm * 1e3, 4)}
+    res["speedup"] = round(per[0] / per[1], 3)
+    return res
 
 
 def run_unfused(args, bufs, P, torch, stream):

@@ -93,10 +93,19 @@ enum {
                                  on the stream) and y_host is not read by such work, so
                                  this call's copies in and convolutions may overlap an
                                  earlier call's copies out                      */
-    PDL_NO_SIMT = 1 << 7      /* GEMM: fail with PDL_EUNSUPPORTED instead of running
+    PDL_NO_SIMT = 1 << 7,     /* GEMM: fail with PDL_EUNSUPPORTED instead of running
                                  the CUDA-core kernel when the operands cannot take the
                                  tensor-core path (unaligned pointers, K = 0, or N /
                                  lda / ldb / ldc not multiples of 4)            */
+    PDL_X_NCHW4C = 1 << 13    /* conv, narrow-channel path only (C <= 4, the ResNet
+                                 stem): x is [N][H][W][4] fp32 (nChw4c with one channel
+                                 block; channels >= C must be finite, their weights are
+                                 zero) instead of nChw16c.  nChw16c stores the stem's 3
+                                 channels in 64-byte pixels and HBM / PCIe move all 64;
+                                 this layout moves the 16 the kernel reads.  Same
+                                 arithmetic in the same order: results are bitwise equal
+                                 to the nChw16c call.  Weights, bias and y are unchanged.
+                                 pdl_pack_nchw4c() produces it from NCHW.        */
 };
 /* Every entry point rejects flag bits it does not implement (PDL_EUNSUPPORTED). */
 
@@ -211,6 +220,8 @@ int pdl_accumulate_epilogue_nchw16c(float *y, const float *y0, const float *bias
  * The reference keeps tensors blocked throughout; these are
  * the pack/unpack steps a PyTorch-layout caller needs before/after it. */
 int pdl_pack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream);
+/* NCHW (C <= 4) -> [N][H][W][4], channels >= C zero: the PDL_X_NCHW4C input layout */
+int pdl_pack_nchw4c(const float *src, float *dst, int N, int C, int H, int W, void *stream);
 int pdl_unpack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream);
 int pdl_pack_kcrs16c16k(const float *src, float *dst, int K, int C, int R, int S, void *stream);
 

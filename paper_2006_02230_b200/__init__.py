@@ -10,7 +10,7 @@ from ._lib import PdlDeviceError, PdlError, PdlShapeError, TileCfg  # noqa: F401
 from . import ops  # noqa: F401
 from .ops import (PackedWeights, SimtPathWarning, accumulate_, bias_relu_, conv2d_nchw,  # noqa: F401
                   conv2d_nchw16c, conv2d_nchw16c_host, conv_out_hw,
-                  device_ok, from_nchw16c, gemm, prepack_weights, to_nchw16c,
+                  device_ok, from_nchw16c, gemm, prepack_weights, to_nchw16c, to_nchw4c,
                   weights_to_kcrs16c16k)
 
 from .loopnest import (LoopDslError, LoopNest, NonAffineError, ParseError, Program,  # noqa: F401

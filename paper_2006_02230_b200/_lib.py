@@ -23,6 +23,7 @@ PDL_MODE_FP32 = 2 << 4
 PDL_MODE_MASK = 3 << 4
 PDL_HOST_X_READY = 1 << 6
 PDL_NO_SIMT = 1 << 7
+PDL_X_NCHW4C = 1 << 13
 PDL_OP_CONV2D = 1
 PDL_OP_GEMM = 2
 
@@ -39,7 +40,7 @@ EXPORTS = (
     "pdl_abi_version", "pdl_device_check", "pdl_pack_nchw16c", "pdl_unpack_nchw16c",
     "pdl_pack_kcrs16c16k", "pdl_conv2d_host_workspace_bytes", "pdl_conv2d_fwd_host",
     "pdl_conv2d_splitk_workspace_bytes", "pdl_conv2d_fwd_prepacked_ws", "pdl_gemm_f32_epilogue",
-    "pdl_accumulate_epilogue_nchw16c", "pdl_conv2d_schedule", "pdl_gemm_schedule",
+    "pdl_accumulate_epilogue_nchw16c", "pdl_conv2d_schedule", "pdl_gemm_schedule", "pdl_pack_nchw4c",
 )
 
 
@@ -97,7 +98,7 @@ _sz = ctypes.c_size_t
 # Entry points an older build may lack (PDL_LIB A/B runs against a previous round's
 # library): declared only when present.
 _OPTIONAL = ("pdl_gemm_f32_epilogue", "pdl_accumulate_epilogue_nchw16c", "pdl_conv2d_schedule",
-             "pdl_gemm_schedule")
+             "pdl_gemm_schedule", "pdl_pack_nchw4c")
 
 
 class _Skip:
@@ -145,6 +146,7 @@ def _declare(L):
     L.pdl_conv2d_schedule.argtypes = [_i] * 9 + [_u, ctypes.POINTER(TileCfg), _i, ctypes.POINTER(Schedule)]
     L.pdl_gemm_schedule.argtypes = [_i, _i, _i, _u, ctypes.POINTER(TileCfg), _i, ctypes.POINTER(Schedule)]
     L.pdl_pack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
+    L.pdl_pack_nchw4c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_unpack_nchw16c.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_pack_kcrs16c16k.argtypes = [_vp, _vp, _i, _i, _i, _i, _vp]
     L.pdl_workspace_bytes.argtypes = [_i, ctypes.POINTER(_i), ctypes.POINTER(TileCfg)]

@@ -144,6 +144,8 @@ constexpr unsigned kDiag = 0;
 #endif
 constexpr unsigned kEpiFlags = PDL_BIAS | PDL_RELU | PDL_RELU6 | PDL_SCALE;
 constexpr unsigned kConvFlags = kEpiFlags | PDL_MODE_MASK;
+// entry points that read x: the compact narrow-channel layout is theirs alone
+constexpr unsigned kConvXFlags = kConvFlags | PDL_X_NCHW4C;
 constexpr unsigned kGemmFlags = kEpiFlags | PDL_MODE_MASK | PDL_NO_SIMT;
 constexpr int kRasterBits = PDL_RASTER_M_FASTEST | PDL_RASTER_BOX_TILES | PDL_RASTER_SEG_TILES | PDL_RASTER_NO_HALO | PDL_RASTER_HALO_CG4;
 
@@ -618,22 +620,29 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     }
     pdl::TmaMaps maps;
     std::memset(&maps, 0, sizeof(maps));
+    // pixel = 16 channels (nChw16c, 64 B, of which the kernel reads the first 16 B) or,
+    // with PDL_X_NCHW4C, exactly the 4 channels it reads (16 B: a quarter of the HBM
+    // and PCIe bytes -- the padded layout makes HBM return the whole 64-byte pixel)
+    const bool compact = (flags & PDL_X_NCHW4C) != 0;
+    const cuuint64_t px = compact ? 16 : 64;  // bytes per pixel
+    const cuuint64_t pc = px / 4;             // floats per pixel
     if (parity) {
         for (int par = 0; par < 2; ++par) {
-            const cuuint64_t dims[5] = {16, (cuuint64_t)((W - par + 1) / 2), (cuuint64_t)H, 1, (cuuint64_t)N};
-            const cuuint64_t str[4] = {128, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
+            const cuuint64_t dims[5] = {pc, (cuuint64_t)((W - par + 1) / 2), (cuuint64_t)H, 1, (cuuint64_t)N};
+            const cuuint64_t str[4] = {2 * px, (cuuint64_t)W * px, (cuuint64_t)H * W * px, (cuuint64_t)H * W * px};
             const cuuint32_t box[5] = {4, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
-            if ((rc = encode(&maps.a[par], x + par * 16, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE,
+            if ((rc = encode(&maps.a[par], x + par * pc, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE,
                              "stem x parity", CU_TENSOR_MAP_L2_PROMOTION_NONE)))
                 return rc;
         }
     } else {
-        const cuuint64_t dims[5] = {16, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
-        const cuuint64_t str[4] = {64, (cuuint64_t)W * 64, (cuuint64_t)H * W * 64, (cuuint64_t)H * W * 64};
+        const cuuint64_t dims[5] = {pc, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
+        const cuuint64_t str[4] = {px, (cuuint64_t)W * px, (cuuint64_t)H * W * px, (cuuint64_t)H * W * px};
         const cuuint32_t box[5] = {4, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
-        // only 16 of every 64 bytes are used: do not promote to 256B L2 fills
+        // nChw16c: only 16 of every 64 bytes are used, do not promote to 256B L2 fills;
+        // compact rows are dense
         if ((rc = encode(&maps.a[0], x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, "stem x",
-                         CU_TENSOR_MAP_L2_PROMOTION_NONE)))
+                         compact ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE)))
             return rc;
     }
     {
@@ -652,7 +661,7 @@ int conv_fwd_stem(const float *x, const float *wp, const float *bias, float *y, 
     p.num_kb = stem_kblocks(C, R, S);
     p.seg_kb = std::max(1, kSegElems / (4 * stem_chunks_per_kb(C, R, S)));
     p.n_out = K;
-    p.flags = flags;
+    p.flags = flags & ~(unsigned)PDL_X_NCHW4C;
     p.bias = bias;
     p.out = y;
     p.nimg = N;
@@ -691,6 +700,9 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
                 size_t *query = nullptr, pdl_schedule *sched = nullptr) {
     int rc;
     if (stride == 2 && (H < 2 || W < 2)) return fail(PDL_EUNSUPPORTED, "conv: stride 2 needs H,W >= 2");
+    if ((flags & PDL_X_NCHW4C) && !is_stem(C, R, S, stride))
+        return fail(PDL_EUNSUPPORTED, "conv: PDL_X_NCHW4C (compact 4-channel x) is the narrow-channel "
+                    "path's layout: C <= 4, S <= 8, R <= %d (got C=%d R=%d S=%d)", pdl::kStemMaxR, C, R, S);
     if (is_stem(C, R, S, stride)) {
         if (query) {
             *query = 0;
@@ -1049,7 +1061,7 @@ int pdl_conv2d_fwd_prepacked(const float *x, const void *packed_w, const float *
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
-    if ((rc = check_flags(flags, kConvFlags, "conv"))) return rc;
+    if ((rc = check_flags(flags, kConvXFlags, "conv"))) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
     if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
         return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
@@ -1078,7 +1090,7 @@ int pdl_conv2d_fwd_prepacked_ws(const float *x, const void *packed_w, const floa
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
-    if ((rc = check_flags(flags, kConvFlags, "conv"))) return rc;
+    if ((rc = check_flags(flags, kConvXFlags, "conv"))) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
     if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
         return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
@@ -1093,7 +1105,7 @@ int pdl_conv2d_schedule(int N, int C, int K, int H, int W, int R, int S, int str
                         unsigned flags, const pdl_tile_cfg *cfg, int with_workspace, pdl_schedule *out) {
     int rc;
     if (!out) return fail(PDL_EINVAL, "schedule: null output");
-    if ((rc = check_flags(flags, kConvFlags, "schedule"))) return rc;
+    if ((rc = check_flags(flags, kConvXFlags, "schedule"))) return rc;
     if ((rc = conv_check(nullptr, nullptr, N, C, K, H, W, R, S, stride, pad))) return rc;
     // a non-null stand-in workspace: auto split-K may engage
     static char ws_token;
@@ -1122,7 +1134,7 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
-    if ((rc = check_flags(flags, kConvFlags | PDL_HOST_X_READY, "conv host"))) return rc;
+    if ((rc = check_flags(flags, kConvXFlags | PDL_HOST_X_READY, "conv host"))) return rc;
     if (!x_host || !y_host) return fail(PDL_EINVAL, "conv host: null host buffer");
     if (chunk < 0) return fail(PDL_EINVAL, "conv host: negative chunk");
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32)
@@ -1142,11 +1154,18 @@ int pdl_conv2d_fwd_host(const float *x_host, const void *packed_w, const float *
     HostPipe *hp;
     if ((rc = host_pipe(workspace, &hp))) return rc;
     const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
-    const size_t x_img = (size_t)ceil16(C) * H * W * 64, y_img = (size_t)(K / 16) * P * Q * 64;
-    const int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
-    const size_t xs = align256(c * x_img);
+    if ((flags & PDL_X_NCHW4C) && !is_stem(C, R, S, stride))
+        return fail(PDL_EUNSUPPORTED, "conv host: PDL_X_NCHW4C needs the narrow-channel path (C <= 4)");
+    // x_host is nChw16c, or [N][H][W][4] with PDL_X_NCHW4C (a quarter of the H2D bytes)
+    const size_t x_img = (flags & PDL_X_NCHW4C) ? (size_t)H * W * 16 : (size_t)ceil16(C) * H * W * 64;
+    const size_t y_img = (size_t)(K / 16) * P * Q * 64;
     uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
     const size_t third = ws_bytes / 3 & ~(size_t)255;
+    int c = chunk > 0 ? std::min(chunk, N) : host_chunk(N, x_img);
+    // (the workspace was sized for nChw16c chunks: the compact layout's larger automatic
+    // chunks must still fit the three x slots)
+    c = (int)std::max<size_t>(1, std::min<size_t>(c, third / kHostSlots / x_img));
+    const size_t xs = align256(c * x_img);
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned cflags = flags & ~(unsigned)PDL_HOST_X_READY;
     // Three internal streams; chunk i uses x slot i % kHostSlots and its own images' place
@@ -1232,12 +1251,14 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
     g_launches = 0;
     int rc;
     if ((rc = device_check())) return rc;
-    if ((rc = check_flags(flags, kConvFlags, "conv"))) return rc;
+    if ((rc = check_flags(flags, kConvXFlags, "conv"))) return rc;
     if ((rc = conv_check(x, y, N, C, K, H, W, R, S, stride, pad))) return rc;
     if ((flags & (PDL_BIAS | PDL_SCALE)) && (!bias || !aligned16(bias)))
         return fail(PDL_EALIGN, "conv: PDL_BIAS / PDL_SCALE need a 16-byte aligned bias");
     cudaStream_t st = (cudaStream_t)stream;
     if ((flags & PDL_MODE_MASK) == PDL_MODE_FP32) {
+        if (flags & PDL_X_NCHW4C)
+            return fail(PDL_EUNSUPPORTED, "conv: PDL_MODE_FP32 reads nChw16c (no PDL_X_NCHW4C)");
         const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
         const long long total = (long long)N * (K / 16) * P * Q;
         pdl::simt_conv_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
@@ -1249,10 +1270,11 @@ int pdl_conv2d_fwd_nchw16c(const float *x, const float *w, const float *bias, fl
     const size_t packed = pdl_conv2d_packed_bytes(C, K, R, S, flags);
     if (!workspace || ws_bytes < packed)
         return fail(PDL_EWORKSPACE, "conv: workspace of %zu bytes required", packed);
+    const unsigned wflags = flags & ~(unsigned)PDL_X_NCHW4C;  // the weight image does not depend on x's layout
     const size_t off = align256(packed);
     void *split_ws = ws_bytes > off ? reinterpret_cast<uint8_t *>(workspace) + off : nullptr;
     const size_t split_bytes = ws_bytes > off ? ws_bytes - off : 0;
-    if ((rc = pdl_conv2d_prepack_weights(w, workspace, C, K, R, S, flags, stream))) return rc;
+    if ((rc = pdl_conv2d_prepack_weights(w, workspace, C, K, R, S, wflags, stream))) return rc;
     rc = conv_fwd_tc(x, reinterpret_cast<const float *>(workspace), bias, y, N, C, K, H, W, R, S,
                      stride, pad, flags, cfg, st, split_ws, split_bytes);
     if (rc == PDL_OK) g_launches = 2;
@@ -1435,6 +1457,22 @@ int pdl_pack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, v
     pdl::pack_nchw16c_kernel<<<grid, pdl::kLayoutThreads, 0, (cudaStream_t)stream>>>(src, dst, N, C, H, W);
     ++g_launches;
     return check_launch("pack_nchw16c_kernel");
+}
+
+int pdl_pack_nchw4c(const float *src, float *dst, int N, int C, int H, int W, void *stream) {
+    g_launches = 0;
+    int rc;
+    if ((rc = layout_check(src, dst, (long long)N | C | H | W))) return rc;
+    if (N <= 0 || C <= 0 || H <= 0 || W <= 0) return fail(PDL_EINVAL, "pack: empty tensor");
+    if (C > 4) return fail(PDL_EINVAL, "pack_nchw4c: C must be <= 4 (got %d)", C);
+    if (!aligned16(dst)) return fail(PDL_EALIGN, "pack: dst must be 16-byte aligned");
+    const long long hw = (long long)H * W;
+    if (N > 65535 || (hw + 255) / 256 > 0x7fffffffLL) return fail(PDL_EUNSUPPORTED, "pack: tensor too large");
+    const dim3 grid((unsigned)((hw + pdl::kLayoutThreads - 1) / pdl::kLayoutThreads), (unsigned)N);
+    pdl::pack_nchw4c_kernel<<<grid, pdl::kLayoutThreads, 0, (cudaStream_t)stream>>>(
+        src, reinterpret_cast<float4 *>(dst), N, C, H, W);
+    ++g_launches;
+    return check_launch("pack_nchw4c_kernel");
 }
 
 int pdl_unpack_nchw16c(const float *src, float *dst, int N, int C, int H, int W, void *stream) {

@@ -32,6 +32,23 @@ __global__ void __launch_bounds__(kLayoutThreads) pack_nchw16c_kernel(const floa
     for (int j = 0; j < 4; ++j) out[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
 
+// src NCHW [N][C][H][W] (C <= 4) -> dst [N][H][W][4] (nChw4c, one channel block),
+// channels >= C zero: the compact input of the narrow-channel conv (PDL_X_NCHW4C).
+// One thread per pixel: C coalesced loads, one float4 store.
+__global__ void __launch_bounds__(kLayoutThreads) pack_nchw4c_kernel(const float *__restrict__ src,
+                                                                     float4 *__restrict__ dst, int N,
+                                                                     int C, int H, int W) {
+    const long long hw = (long long)H * W;
+    const long long pix = (long long)blockIdx.x * kLayoutThreads + threadIdx.x;
+    const int n = blockIdx.y;
+    if (pix >= hw) return;
+    const float *in = src + (size_t)n * C * hw + pix;
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = c < C ? __ldg(in + (size_t)c * hw) : 0.f;
+    dst[(size_t)n * hw + pix] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
 // src nChw16c [N][ceil(C/16)][H][W][16] -> dst NCHW [N][C][H][W] (padding channels dropped)
 __global__ void __launch_bounds__(kLayoutThreads) unpack_nchw16c_kernel(const float *__restrict__ src,
                                                                         float *__restrict__ dst, int N,

@@ -3,6 +3,8 @@ current CUDA stream; all arithmetic runs in libpdl.so kernels.
 
 Layouts (the reference nest's array declarations):
   x  [N][C/16][H][W][16]          nChw16c activations, UNPADDED
+     [N][H][W][4]                 compact narrow-channel input (C <= 4, the ResNet stem):
+                                  a 4-D x selects PDL_X_NCHW4C (to_nchw4c() makes it)
   w  [K/16][C/16][R][S][16c][16k]  KCRS16c16k weights
   y  [N][K/16][P][Q][16]           nKhw16k outputs
   bias [K]
@@ -18,7 +20,7 @@ import torch
 
 from . import _lib
 from ._lib import (PDL_BIAS, PDL_HOST_X_READY, PDL_MODE_FP32, PDL_NO_SIMT, PDL_OP_GEMM, PDL_RELU,
-                   PDL_RELU6, PDL_SCALE, MODES, TileCfg, check, lib)
+                   PDL_RELU6, PDL_SCALE, PDL_X_NCHW4C, MODES, TileCfg, check, lib)
 
 
 class SimtPathWarning(UserWarning):
@@ -155,9 +157,7 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
     kernel)."""
     _need_cuda_f32("x", x)
     _need_cuda_f32("bias", bias)
-    n, ct, h, wd, v = x.shape
-    if v != 16:
-        raise ValueError("x must be nChw16c")
+    n, ct, h, wd, compact = _x_dims(x)
     packed = w if isinstance(w, PackedWeights) else None
     if packed is not None:
         C, K, R, S = packed.C, packed.K, packed.R, packed.S
@@ -171,19 +171,35 @@ def conv2d_nchw16c(x: torch.Tensor, w, bias: torch.Tensor | None = None, stride:
         raise ValueError(f"channels={channels} but weights were packed for C={C}")
     if not (ct * 16 - 16 < C <= ct * 16):
         raise ValueError(f"channel mismatch: x has {ct} blocks of 16, w has C={C}")
+    if compact and C > 4:
+        raise ValueError(f"a 4-D x is the compact [N][H][W][4] layout (C <= 4); weights have C={C}")
     P, Q = conv_out_hw(h, wd, R, S, stride, pad)
     with _on(stream):
         return _conv2d_call(x, w, packed, bias, out, n, C, K, h, wd, R, S, P, Q, stride, pad, relu,
-                            relu6, scale, mode, cfg, stream)
+                            relu6, scale, mode, cfg, stream, PDL_X_NCHW4C if compact else 0)
+
+
+def _x_dims(x):
+    """(N, channel blocks, H, W, compact) of a conv input: 5-D nChw16c, or the 4-D
+    compact [N][H][W][4] layout of the narrow-channel path."""
+    if x.dim() == 4:
+        n, h, wd, v = x.shape
+        if v != 4:
+            raise ValueError("a 4-D x must be [N][H][W][4] (compact narrow-channel layout)")
+        return n, 1, h, wd, True
+    n, ct, h, wd, v = x.shape
+    if v != 16:
+        raise ValueError("x must be nChw16c")
+    return n, ct, h, wd, False
 
 
 def _conv2d_call(x, w, packed, bias, out, n, C, K, h, wd, R, S, P, Q, stride, pad, relu, relu6,
-                 scale, mode, cfg, stream):
+                 scale, mode, cfg, stream, xflags=0):
     y = out if out is not None else torch.empty((n, K // 16, P, Q, 16), dtype=torch.float32,
                                                 device=x.device)
     _need_cuda_f32("out", y)
     eflags, bias = _epilogue(bias, relu, relu6, scale, K)
-    flags = _mode(mode) | eflags
+    flags = _mode(mode) | eflags | xflags
     st = ctypes.c_void_p(_stream(stream))
     cp = _cfg_ptr(cfg)
     if packed is not None:
@@ -243,9 +259,9 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     _need_cuda_f32("bias", bias)
     if w.mode != mode.lower():
         raise ValueError(f"weights packed for {w.mode}, called with {mode}")
-    n, ct, h, wd, v = x.shape
-    if v != 16 or not (ct * 16 - 16 < w.C <= ct * 16):
-        raise ValueError(f"x must be nChw16c with {w.C} channels")
+    n, ct, h, wd, compact = _x_dims(x)
+    if not (ct * 16 - 16 < w.C <= ct * 16) or (compact and w.C > 4):
+        raise ValueError(f"x must be nChw16c (or, for C <= 4, [N][H][W][4]) with {w.C} channels")
     P, Q = conv_out_hw(h, wd, w.R, w.S, stride, pad)
     y = out if out is not None else torch.empty((n, w.K // 16, P, Q, 16), dtype=torch.float32,
                                                 pin_memory=True)
@@ -258,7 +274,7 @@ def conv2d_nchw16c_host(x: torch.Tensor, w: PackedWeights, bias: torch.Tensor | 
     ws = _host_workspace(dev, sh, need)
     with _on(stream):
         eflags, bias = _epilogue(bias, relu, relu6, scale, w.K)
-    flags = _mode(mode) | eflags
+    flags = _mode(mode) | eflags | (PDL_X_NCHW4C if compact else 0)
     if x_ready and scale is None:   # (a fused scale builds its [shift | scale] buffer on `stream`)
         flags |= PDL_HOST_X_READY
     check(lib().pdl_conv2d_fwd_host(_ptr(x), _ptr(w.data), _ptr(bias), _ptr(y), n, w.C, w.K, h, wd,
@@ -350,6 +366,20 @@ def to_nchw16c(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) ->
     return out
 
 
+def to_nchw4c(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """NCHW with C <= 4 -> the compact [N][H][W][4] input of the narrow-channel conv
+    (channels >= C zero); conv2d_nchw16c / conv2d_nchw16c_host take it as a 4-D x."""
+    x = x.contiguous()
+    _need_cuda_f32("x", x)
+    n, c, h, w = x.shape
+    if c > 4:
+        raise ValueError(f"to_nchw4c: C must be <= 4, got {c}")
+    if out is None:
+        out = torch.empty((n, h, w, 4), dtype=torch.float32, device=x.device)
+    check(lib().pdl_pack_nchw4c(_ptr(x), _ptr(out), n, c, h, w, ctypes.c_void_p(_stream(stream))))
+    return out
+
+
 def from_nchw16c(y: torch.Tensor, channels: int | None = None, out: torch.Tensor | None = None,
                  stream=None) -> torch.Tensor:
     """nChw16c -> NCHW, dropping padding channels beyond `channels`."""
@@ -392,5 +422,5 @@ def device_ok() -> bool:
 
 
 __all__ = ["conv2d_nchw16c", "prepack_weights", "PackedWeights", "gemm", "bias_relu_", "accumulate_",
-           "device_ok", "conv_out_hw", "TileCfg", "SimtPathWarning"]
+           "device_ok", "conv_out_hw", "TileCfg", "SimtPathWarning", "to_nchw4c"]
 _ = _lib
