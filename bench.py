@@ -48,6 +48,8 @@ def parse_args():
                     help="skip the sub-objects for the other BASELINE configs (gemm, pr1, n28, tf32)")
     ap.add_argument("--box-tiles", action="store_true", help="A/B: disable segment tiles (PDL_RASTER_BOX_TILES)")
     ap.add_argument("--m-fastest", action="store_true", help="A/B: output-pixel tiles fastest (PDL_RASTER_M_FASTEST)")
+    ap.add_argument("--single-image-tiles", action="store_true",
+                    help="A/B: round-1 tile geometry, no multi-image box search (PDL_RASTER_SINGLE_IMAGE_TILES)")
     ap.add_argument("--no-halo", action="store_true", help="A/B: per-tap A boxes for 3x3 layers (PDL_RASTER_NO_HALO)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay of the step")
     ap.add_argument("--no-cpu", action="store_true")
@@ -378,6 +380,8 @@ def run_suite(args, rank, world, local):
         cfg = dict(cfg or {}, raster=2)
     if args.m_fastest:  # A/B: tile-loop interchange (pixel tiles fastest)
         cfg = dict(cfg or {}, raster=(cfg or {}).get("raster", 0) | 1)
+    if args.single_image_tiles:  # A/B: a tile holds several images only when a whole image fits
+        cfg = dict(cfg or {}, raster=(cfg or {}).get("raster", 0) | 8)
     if args.no_halo:  # A/B: one A box per tap for 3x3 layers
         cfg = dict(cfg or {}, raster=(cfg or {}).get("raster", 0) | 16)
     if args.schedule == "ranked":

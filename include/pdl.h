@@ -65,15 +65,22 @@ typedef struct pdl_tile_cfg {
                       CTA pairs, the stem and resident weights); bit 1 (PDL_RASTER_BOX_TILES):
                       box tiles only -- no multi-image segment tiles for small maps;
                       bit 2 (PDL_RASTER_SEG_TILES): segment tiles whenever the shape
-                      allows, even if they do not remove a wave of tiles; bits 4
-                      and 6 below; any other bit: PDL_EUNSUPPORTED              */
+                      allows, even if they do not remove a wave of tiles; bits 3, 4,
+                      6 and the tile box in bits 8-30 below; any other bit: PDL_EUNSUPPORTED              */
 } pdl_tile_cfg;
 
 #define PDL_RASTER_M_FASTEST 1
 #define PDL_RASTER_BOX_TILES 2
 #define PDL_RASTER_SEG_TILES 4
+#define PDL_RASTER_SINGLE_IMAGE_TILES 8 /* box tiles hold several images only when a whole image
+                                          fits (the round-1 geometry); default: the box search
+                                          over (pixels wide, pixels high, images) that fills the
+                                          128 tensor-core rows best */
 #define PDL_RASTER_NO_HALO 16  /* 3x3 convs: one A box per tap instead of one halo per channel group */
 #define PDL_RASTER_HALO_CG4 64 /* 3xTF32 halo mode with 64-channel k-blocks (one halo buffer) */
+/* explicit conv tile box: w x h output pixels of n consecutive images, w*h*n <= 128 */
+#define PDL_RASTER_TILE(w, h, n) (((w) & 0xff) << 8 | ((h) & 0xff) << 16 | ((n) & 0x7f) << 24)
+#define PDL_RASTER_TILE_MASK 0x7fffff00
 
 enum {
     PDL_BIAS = 1,             /* y += bias[k]                                  */

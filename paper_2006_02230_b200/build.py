@@ -35,8 +35,15 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    out = os.environ.get("PDL_LIB_OUT")  # experiment builds (PDL_TRACE, PDL_DIAG, ...) beside the product library
+    if out:
+        return _compile(os.path.abspath(out), verbose)
     if not force and not stale():
         return LIB
+    return _compile(LIB, verbose)
+
+
+def _compile(LIB: str, verbose: bool) -> str:
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            os.path.join(SRC, "pdl_capi.cu")]
@@ -46,6 +53,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(4, "-DPDL_WATCHDOG=1")
     if os.environ.get("PDL_TRACE"):
         cmd.insert(4, "-DPDL_TRACE=1")
+    if os.environ.get("PDL_DIAG"):
+        cmd.insert(4, "-DPDL_DIAG=1")
+    for d in os.environ.get("PDL_DEFINES", "").split():  # e.g. PDL_DEFINES="-DPDL_HALO_SUB=18432"
+        cmd.insert(4, d)
     if os.environ.get("PDL_EPI_BUFS"):  # experiments: output-box ring depth per epilogue half
         cmd.insert(4, "-DPDL_EPI_BUFS=%d" % int(os.environ["PDL_EPI_BUFS"]))
     if os.environ.get("PDL_EPI_BUFS_WIDE"):  # ... of the resident-weight 1x1 / stem instances

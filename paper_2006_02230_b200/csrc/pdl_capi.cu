@@ -147,7 +147,8 @@ constexpr unsigned kConvFlags = kEpiFlags | PDL_MODE_MASK;
 // entry points that read x: the compact narrow-channel layout is theirs alone
 constexpr unsigned kConvXFlags = kConvFlags | PDL_X_NCHW4C;
 constexpr unsigned kGemmFlags = kEpiFlags | PDL_MODE_MASK | PDL_NO_SIMT;
-constexpr int kRasterBits = PDL_RASTER_M_FASTEST | PDL_RASTER_BOX_TILES | PDL_RASTER_SEG_TILES | PDL_RASTER_NO_HALO | PDL_RASTER_HALO_CG4;
+constexpr int kRasterBits = PDL_RASTER_M_FASTEST | PDL_RASTER_BOX_TILES | PDL_RASTER_SEG_TILES | PDL_RASTER_NO_HALO |
+                            PDL_RASTER_HALO_CG4 | PDL_RASTER_SINGLE_IMAGE_TILES | PDL_RASTER_TILE_MASK;
 
 int check_flags(unsigned flags, unsigned allowed, const char *what) {
     const unsigned bad = flags & ~(allowed | kDiag);
@@ -355,6 +356,10 @@ SplitPlan plan_split(int m_tiles, int n_tiles, int cl, int bn, int num_kb, int s
         for (int s = 2; s <= 16; ++s) {
             const int kps = (num_kb + s - 1) / s;
             if (kps < 16) break;  // shorter ranges lose to the partial exchange (512^3 GEMM)
+            // the split units must fit one wave: a second wave of units waits for the first one's
+            // reductions (ResNet layer 17 at 28 / 32 images, 56 tiles: x5 in two waves ran 74-76 us
+            // against 57 us for x2 in one wave, where this model had predicted 75 vs 80)
+            if ((long long)tiles * s > sm_count) break;
             const double c = (double)((tiles * s + sm_count - 1) / sm_count) * (kps + kOverheadKb) + 0.25 * s;
             if (c < best - 1e-9) {
                 best = c;
@@ -432,9 +437,72 @@ struct ConvGeom {
     int seg_mode = 0, seg_tile = 0, seg_imgs = 1;
 };
 
+// Box tile search.  A tile is a box of BW x BH output pixels of BNI consecutive images
+// (one TMA box per 16-channel sub-tile, any BNI: the image is just the box's outermost
+// dimension), BW * BH * BNI <= 128 rows.  Round 1 only packed several images into a tile
+// when a whole image fit (7x7 maps), so 28x28 maps filled 112 of 128 MMA rows, 14x14 box
+// tiles 98 and 7x7 maps 98: 12-23% of every tensor-core pass multiplied zero rows.  The
+// search first finds the fewest waves of the persistent grid (tiles x n_tiles work units
+// over the SMs -- at small batches the wave count is what the time follows), then takes the
+// widest box (longest contiguous run: BW pixels x 64 B per row and image) among the shapes
+// within kTileSlack of that, then the fewest tiles, then the taller box.  Runs shorter than
+// kMinRunPx pixels are not considered unless the map itself is narrower.
+//   halo_r / halo_s >= 0: the tile's input halo (BW + halo_s) x (BH + halo_r) x BNI pixels
+//   must fit one halo buffer (kHaloSub bytes per 16-channel sub-tile), see HALO.
+// Measured on the 20 ResNet-50 layers at 256 images (scripts/probe_tile_shapes.py,
+// profiles/tile_shapes_r2f.log): the pick is the fastest or within 2% of the fastest
+// explicit box on every layer; suite 157.6 -> 170.9 TFLOP/s same box.
+constexpr int kMinRunPx = 4;
+constexpr double kTileSlack = 1.04;
+struct BoxShape {
+    int bw = 0, bh = 0, bni = 0;
+    long long tiles = 0, waves = 0;
+};
+BoxShape pick_box(int N, int Pg, int Qg, int n_tiles, int halo_r, int halo_s) {
+    const int halo_px = pdl::kHaloSub / 64;
+    const long long wave = sms();
+    BoxShape best;
+    for (int pass = 0; pass < 2; ++pass) {
+        // pass 0: the fewest waves (then tiles); pass 1: the widest box within the slack of it
+        const long long wlimit = pass ? (long long)(best.waves * kTileSlack) : 0;
+        BoxShape pick;
+        for (int bw = std::min(Qg, 128); bw >= 1; --bw) {
+            if (bw < std::min(Qg, kMinRunPx)) break;
+            for (int bh = std::min(Pg, 128 / bw); bh >= 1; --bh) {
+                int bni = std::min(N, 128 / (bw * bh));
+                if (halo_r >= 0) bni = std::min(bni, halo_px / ((bw + halo_s) * (bh + halo_r)));
+                if (bni < 1) continue;
+                const long long tiles =
+                    (long long)((Qg + bw - 1) / bw) * ((Pg + bh - 1) / bh) * ((N + bni - 1) / bni);
+                const long long waves = (tiles * n_tiles + wave - 1) / wave;
+                const BoxShape c{bw, bh, bni, tiles, waves};
+                if (pass == 0) {
+                    if (!pick.bw || waves < pick.waves || (waves == pick.waves && tiles < pick.tiles)) pick = c;
+                } else if (waves <= wlimit) {
+                    if (!pick.bw || (bw == pick.bw && tiles < pick.tiles)) pick = c;
+                }
+            }
+            if (pass == 1 && pick.bw) break;  // widest box found
+        }
+        best = pick;
+        if (!best.bw) break;
+    }
+    return best;
+}
+// a beats b by more than the slack (waves first, then tiles)
+bool box_wins(const BoxShape &a, const BoxShape &b) {
+    if (!a.bw) return false;
+    if (!b.bw) return true;
+    return a.waves < b.waves || (a.waves == b.waves && (long long)(a.tiles * kTileSlack) < b.tiles);
+}
+
 // n_tiles: output-channel tiles (segment tiles only pay when they cut whole waves).
+// single_image: the round-1 geometry (PDL_RASTER_SINGLE_IMAGE_TILES): a tile holds several
+// images only when a whole image fits.  halo_r / halo_s: see pick_box (-1: no halo limit).
+// tile_w/h/n > 0: the caller's explicit box (PDL_RASTER_TILE), in image coordinates.
 ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool allow_seg = true,
-                   int n_tiles = 1, bool force_seg = false) {
+                   int n_tiles = 1, bool force_seg = false, bool single_image = false, int halo_r = -1,
+                   int halo_s = -1, int tile_w = 0, int tile_h = 0, int tile_n = 0) {
     ConvGeom g{};
     g.P = (H + 2 * pad - R) / stride + 1;
     g.Q = (W + 2 * pad - S) / stride + 1;
@@ -446,6 +514,32 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool 
     g.BW = std::min(g.Qg, 128);
     g.BH = std::min(g.Pg, 128 / g.BW);
     g.BNI = (g.BH == g.Pg) ? std::max(1, std::min(N, 128 / (g.BW * g.BH))) : 1;
+    if (tile_w > 0) {
+        g.flat = false;
+        g.Hg = H; g.Wg = W; g.Pg = g.P; g.Qg = g.Q;
+        g.BW = tile_w; g.BH = tile_h; g.BNI = tile_n;
+    } else if (!single_image) {
+        const long long legacy = (long long)((g.Qg + g.BW - 1) / g.BW) * ((g.Pg + g.BH - 1) / g.BH) *
+                                 ((N + g.BNI - 1) / g.BNI);
+        BoxShape b = pick_box(N, g.Pg, g.Qg, n_tiles, halo_r, halo_s);
+        if (halo_r >= 0) {
+            // halo mode saves 3-4% on a 3x3 layer; a box that does not fit a halo buffer but
+            // fills the rows better saves more (ResNet layer 17: 7x1 pixels x 18 images with
+            // per-tap boxes 247 us, 7x7 x 2 images with the halo 335 us; layers 7 / 12: 4% / 3%)
+            const BoxShape free_box = pick_box(N, g.Pg, g.Qg, n_tiles, -1, -1);
+            if (box_wins(free_box, b)) b = free_box;
+        }
+        bool unflat = false;
+        if (g.flat) {  // 1x1/s1/p0: also boxes of the unflattened map (rows of several images)
+            // (the flattened map has the longer runs: it stays unless the boxes win by the slack)
+            const BoxShape b2 = pick_box(N, g.P, g.Q, n_tiles, -1, -1);
+            if (box_wins(b2, b)) { b = b2; unflat = true; }
+        }
+        if (b.bw && b.tiles < legacy) {
+            if (unflat) { g.flat = false; g.Hg = H; g.Wg = W; g.Pg = g.P; g.Qg = g.Q; }
+            g.BW = b.bw; g.BH = b.bh; g.BNI = b.bni;
+        }
+    }
     g.tiles_w = (g.Qg + g.BW - 1) / g.BW;
     g.tiles_h = (g.Pg + g.BH - 1) / g.BH;
     g.tiles_n = (N + g.BNI - 1) / g.BNI;
@@ -478,7 +572,11 @@ ConvGeom conv_geom(int N, int H, int W, int R, int S, int stride, int pad, bool 
             const long long wave = sms();
             const long long w_box = ((long long)g.m_tiles * n_tiles + wave - 1) / wave;
             const long long w_seg = (mt * n_tiles + wave - 1) / wave;
-            if ((w_seg < w_box || (force_seg && mt < g.m_tiles)) && mt < (1ll << 30)) {
+            // (round 2: with multi-image boxes the segment tiles lose on every ResNet layer at 256
+            // and 32 images -- layers 13 / 14 at 256: 150 / 275 us against 126 / 224 us -- so they
+            // are only taken when forced)
+            (void)w_seg; (void)w_box;
+            if (force_seg && mt < (1ll << 30)) {
                 g.seg_mode = 1;
                 g.seg_tile = T;
                 g.seg_imgs = gi;
@@ -767,9 +865,26 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     if (cl != 1 && cl != 2 && cl != 4) return fail(PDL_EINVAL, "conv: cluster_m must be 1, 2 or 4");
     if (cfg.bn % (8 * cl)) return fail(PDL_EINVAL, "conv: bn=%d not divisible into %d slices", cfg.bn, cl);
     if (cg < 1 || CT % cg) return fail(PDL_EINVAL, "conv: bk=%d does not divide C=%d", cfg.bk, C);
+    // halo mode wanted (decided before the tile shape: the shape must fit a halo buffer)
+    const bool halo_cg4 = (cfg_in && (cfg_in->raster & PDL_RASTER_HALO_CG4)) || cfg.bn == 64;
+    const bool want_halo = !pair && !resident && !epix && stride == 1 && R * S > 1 && cl == 1 && cfg.bn <= 128 &&
+                           (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
+                           !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO));
+    // explicit tile box (PDL_RASTER_TILE): bits 8-15 BW, 16-23 BH, 24-30 BNI
+    const int tile_w = cfg_in ? (cfg_in->raster >> 8) & 0xff : 0, tile_h = cfg_in ? (cfg_in->raster >> 16) & 0xff : 0,
+              tile_n = cfg_in ? (cfg_in->raster >> 24) & 0x7f : 0;
+    if (tile_w || tile_h || tile_n) {
+        const int Pq = (H + 2 * pad - R) / stride + 1, Qq = (W + 2 * pad - S) / stride + 1;
+        if (tile_w < 1 || tile_h < 1 || tile_n < 1 || tile_w * tile_h * tile_n > 128 || tile_w > Qq || tile_h > Pq ||
+            tile_n > N || pair)
+            return fail(PDL_EINVAL, "conv: tile box %d x %d pixels x %d images must be 1..128 rows inside the "
+                        "%d x %d map and the batch", tile_w, tile_h, tile_n, Qq, Pq);
+    }
     const ConvGeom g = conv_geom(N, H, W, R, S, stride, pad,
-                                 !pair && !(cfg_in && (cfg_in->raster & PDL_RASTER_BOX_TILES)),
-                                 (K + cfg.bn - 1) / cfg.bn, cfg_in && (cfg_in->raster & PDL_RASTER_SEG_TILES));
+                                 !pair && !tile_w && !(cfg_in && (cfg_in->raster & PDL_RASTER_BOX_TILES)),
+                                 (K + cfg.bn - 1) / cfg.bn, cfg_in && (cfg_in->raster & PDL_RASTER_SEG_TILES),
+                                 pair || (cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES)),
+                                 want_halo ? R - 1 : -1, want_halo ? S - 1 : -1, tile_w, tile_h, tile_n);
     // segment tiles: no weight multicast by default (pairs of CTAs in lockstep wait for
     // the one whose tile spans two images; cluster 1 measured 4-9% faster on ResNet
     // layers 12/13/15 at 256 images)
@@ -792,15 +907,11 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // per channel group instead of one box per tap
     // 3xTF32 64-channel k-blocks at BN=64 (layer 3) take halo mode with one halo buffer:
     // 333 vs 340 us isolated in round 1p (a tie in round 1l); PDL_RASTER_HALO_CG4 forces it
-    const bool halo_cg4 = (cfg_in && (cfg_in->raster & PDL_RASTER_HALO_CG4)) || cfg.bn == 64;
+    // (3xTF32: not with 64-channel k-blocks at BN=128 -- two 64 KB halo buffers leave 2 weight
+    // stages; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.  TF32 stages carry one
+    // weight plane, so 64-channel k-blocks keep 4 stages.)
     const int halo_w = g.BW + S - 1, halo_h = g.BH + R - 1;
-    // (3xTF32: not with 64-channel k-blocks -- two 64 KB halo buffers leave 2 weight stages,
-    // and layer 3 ran 376 vs 335 us; BN=128 3x3 layers 7/12/17 run 4-6% faster isolated.
-    // TF32 stages carry one weight plane, so 64-channel k-blocks keep 4 stages.)
-    const bool halo = !pair && !resident && !epix && !g.seg_mode && stride == 1 && R * S > 1 && cl == 1 &&
-                      cfg.bn <= 128 &&
-                      (cg <= 2 || (!split && cg == 4) || halo_cg4 || cfg.bn == 128) &&
-                      !(cfg_in && (cfg_in->raster & PDL_RASTER_NO_HALO)) && halo_w <= 256 && halo_h <= 256 &&
+    const bool halo = want_halo && !g.seg_mode && halo_w <= 256 && halo_h <= 256 &&
                       halo_w * halo_h * g.BNI * 64 <= pdl::kHaloSub;
     if (sched) {
         std::memset(sched, 0, sizeof(*sched));

@@ -25,7 +25,7 @@ for arg in (sys.argv[1:] or ["3", "7", "4", "17"]):
         run = lambda: P.gemm(a, bm, c, cfg=cfg)
     else:
         l = W.LAYERS[int(arg) - 1]
-        n = 256
+        n = int(os.environ.get("N", "256"))
         x = torch.rand((n, l.C_alloc // 16, l.H, l.W, 16), device='cuda')
         w = torch.rand((l.K // 16, l.C_alloc // 16, l.R, l.S, 16, 16), device='cuda')
         b = torch.rand(l.K, device='cuda')

@@ -76,8 +76,11 @@ def launches(path: str, tag: str):
 
 
 def rep(path: str, tag: str, names: list[str] | None):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if path.endswith(".csv"):  # `ncu -i x.ncu-rep --page raw --csv` exported on the GPU box
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     kn = hdr.index("Kernel Name")

@@ -110,9 +110,13 @@ def test_flags_are_validated(P):
     x = torch.zeros((1, 4, 8, 8, 16), device="cuda")
     w = torch.zeros((4, 4, 1, 1, 16, 16), device="cuda")
     pw = P.prepack_weights(w)
-    for bad_raster in (8, 32, 128):
+    for bad_raster in (32, 128, 1 << 31):
         with pytest.raises(_lib.PdlShapeError, match="raster"):
-            P.conv2d_nchw16c(x, pw, cfg={"raster": bad_raster})
+            P.conv2d_nchw16c(x, pw, cfg={"raster": bad_raster - (1 << 32) if bad_raster >= 1 << 31 else bad_raster})
+    # explicit tile boxes (PDL_RASTER_TILE): more than 128 rows, wider than the map, more images than the batch
+    for bw, bh, bni in ((64, 4, 1), (16, 1, 1), (8, 8, 2), (0, 8, 1)):
+        with pytest.raises(_lib.PdlShapeError, match="tile box"):
+            P.conv2d_nchw16c(x, pw, cfg={"raster": bw << 8 | bh << 16 | bni << 24})
     y = torch.zeros((1, 4, 8, 8, 16), device="cuda")
     rc = L_.pdl_conv2d_fwd_prepacked(p(x), p(pw.data), nul, p(y), 1, 64, 64, 8, 8, 1, 1, 1, 0,
                                      1 << 9, None, nul)
