@@ -112,6 +112,9 @@ enum TraceEv {
     TR_E_STORED,      // epilogue: tile j stored
     TR_M_WAITED,      // MMA: barrier observed (before tcgen05.fence::after_thread_sync)
     TR_M_LOOP,        // MMA: top of k-block loop
+    TR_KERNEL,        // [0] kernel entry, [1] prologue done (barriers, TMEM), [2] after griddepcontrol.wait,
+                      // [3] before the final CTA sync (warp 8 lane 0), [4] after TMEM dealloc
+    TR_SPLIT,         // split-K, per unit j: [2j] partial written + counter bumped, [2j+1] reduction read back
     TR_COUNT
 };
 __device__ __forceinline__ void trace_ev(const TileParams &p, int ev, int i) {
@@ -510,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) trace_ev(p, TR_KERNEL, 0);
     const int num_tiles = p.m_tiles * p.n_tiles;
     const int seg_kb = p.seg_kb;
     // Cluster of CL CTAs = CL consecutive M-tiles of one N-tile ("super-tile"),
@@ -563,6 +567,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (PAIR) tmem_alloc2<L::TMEM_COLS>(tmem_slot);
         else tmem_alloc<L::TMEM_COLS>(tmem_slot);
     }
+    if (warp == 3) {
+        // the otherwise idle warp touches every word of the geometry parameters, so the
+        // constant-bank lines the producer's first tile_coord needs are resident when the
+        // prologue ends (timelines of short launches: 2200 cycles from the end of the
+        // prologue to the first TMA issue, mostly a chain of constant-cache misses)
+        const unsigned *pw = reinterpret_cast<const unsigned *>(&p);
+        unsigned acc = 0;
+        for (int i = lane; i < (int)(sizeof(TileParams) / 4); i += 32) acc += pw[i];
+        asm volatile("" ::"r"(acc));
+    }
     tc_fence_before();
     if (CL > 1) cluster_sync();  // peers multicast into our barriers: they must exist
     else __syncthreads();
@@ -570,8 +584,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // programmatic dependent launch: let the next kernel on the stream start its own
     // prologue now, and touch global memory only once the previous grid has finished
     // (a no-op when launched without the attribute)
+    if (threadIdx.x == 0) trace_ev(p, TR_KERNEL, 1);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) trace_ev(p, TR_KERNEL, 2);
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t smem0 = smem_u32(smem);
 
@@ -1221,15 +1237,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // split: 122.9 us vs 122.1 with this rule -- so the simpler rule stays.
                 // Splits pay only for long ranges; plan_split asks for >= 16 k-blocks.)
                 const int tile = tile_of(st_i);
+                // partial layout [16-column block][float4 of the block][128 rows][4]: a warp's 32
+                // rows of one float4 are 512 contiguous bytes, for the write and the read back
+                auto poff = [&](int j, int q4) { return (((half * (HALF / 16) + j) * 4 + q4) * 128 + row) * 4; };
                 float *mine = p.part + ((size_t)tile * SPL + sp) * (128 * BN);
 #pragma unroll
-                for (int j = 0; j < HALF / 16; ++j) {
-                    float4 *d = reinterpret_cast<float4 *>(mine + ((half * (HALF / 16) + j) * 128 + row) * 16);
+                for (int j = 0; j < HALF / 16; ++j)
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4)
-                        d[q4] = make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1],
-                                            sum[j * 16 + q4 * 4 + 2], sum[j * 16 + q4 * 4 + 3]);
-                }
+                        *reinterpret_cast<float4 *>(mine + poff(j, q4)) =
+                            make_float4(sum[j * 16 + q4 * 4], sum[j * 16 + q4 * 4 + 1], sum[j * 16 + q4 * 4 + 2],
+                                        sum[j * 16 + q4 * 4 + 3]);
                 __threadfence();
                 named_bar_sync(4, kEpiThreads);
                 if (e == 0 && lane == 0) {
@@ -1239,26 +1257,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *split_flag = last;
                 }
                 named_bar_sync(4, kEpiThreads);
+                if (tr) trace_ev(p, TR_SPLIT, 2 * jt);
                 if (!*split_flag) continue;
                 __threadfence();
-                // fixed split order (independent of arrival order): ((p0 + p1) + p2) + ...;
-                // this unit's own partial is read back too (registers stay free).  Loads are
-                // batched (all of p0, then 8 float4 of each later partial at a time): one
-                // dependent L2 round trip per batch, not per 16 columns and partial (L18 at
-                // 32 images: 4-way split 131.8 -> 122.1 us, 8-way 530 -> 432 us)
                 const float *tp = p.part + (size_t)tile * SPL * (128 * BN);
-                auto poff = [&](int j) { return ((half * (HALF / 16) + j) * 128 + row) * 16; };
-#pragma unroll
-                for (int j = 0; j < HALF / 16; ++j)
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        const float4 v4 = __ldcg(reinterpret_cast<const float4 *>(tp + poff(j)) + q4);
-                        sum[j * 16 + q4 * 4] = v4.x; sum[j * 16 + q4 * 4 + 1] = v4.y;
-                        sum[j * 16 + q4 * 4 + 2] = v4.z; sum[j * 16 + q4 * 4 + 3] = v4.w;
-                    }
-#pragma unroll 1
-                for (int q = 1; q < SPL; ++q) {
-                    const float *src = tp + (size_t)q * (128 * BN);
+                if (SPL == 2) {
+                    // two ranges: p0 + p1 is the same sum whichever unit arrives last, so the
+                    // reducer keeps its own range in registers and reads only the other one
+                    // (fp32 addition commutes exactly, so the result is bitwise the general path's)
+                    const float *src = tp + (size_t)(sp ^ 1) * (128 * BN);
 #pragma unroll
                     for (int j0 = 0; j0 < HALF / 16; j0 += 2) {
                         float4 w4[2][4];
@@ -1267,7 +1274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int q4 = 0; q4 < 4; ++q4)
                                 w4[jj][q4] = (j0 + jj < HALF / 16)
-                                                 ? __ldcg(reinterpret_cast<const float4 *>(src + poff(j0 + jj)) + q4)
+                                                 ? __ldcg(reinterpret_cast<const float4 *>(src + poff(j0 + jj, q4)))
                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int jj = 0; jj < 2; ++jj) {
@@ -1280,8 +1287,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
+                } else {
+                    // fixed split order (independent of arrival order): ((p0 + p1) + p2) + ...;
+                    // this unit's own partial is read back too.  Loads are batched (all of p0, then
+                    // 8 float4 of each later partial at a time): one dependent L2 round trip per
+                    // batch, not per 16 columns and partial (L18 at 32 images: 4-way split
+                    // 131.8 -> 122.1 us, 8-way 530 -> 432 us)
+#pragma unroll
+                    for (int j = 0; j < HALF / 16; ++j)
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            const float4 v4 = __ldcg(reinterpret_cast<const float4 *>(tp + poff(j, q4)));
+                            sum[j * 16 + q4 * 4] = v4.x; sum[j * 16 + q4 * 4 + 1] = v4.y;
+                            sum[j * 16 + q4 * 4 + 2] = v4.z; sum[j * 16 + q4 * 4 + 3] = v4.w;
+                        }
+#pragma unroll 1
+                    for (int q = 1; q < SPL; ++q) {
+                        const float *src = tp + (size_t)q * (128 * BN);
+#pragma unroll
+                        for (int j0 = 0; j0 < HALF / 16; j0 += 2) {
+                            float4 w4[2][4];
+#pragma unroll
+                            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; ++q4)
+                                    w4[jj][q4] = (j0 + jj < HALF / 16)
+                                                     ? __ldcg(reinterpret_cast<const float4 *>(src + poff(j0 + jj, q4)))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                            for (int jj = 0; jj < 2; ++jj) {
+                                if (j0 + jj >= HALF / 16) break;
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; ++q4) {
+                                    float *d = &sum[(j0 + jj) * 16 + q4 * 4];
+                                    d[0] += w4[jj][q4].x; d[1] += w4[jj][q4].y;
+                                    d[2] += w4[jj][q4].z; d[3] += w4[jj][q4].w;
+                                }
+                            }
+                        }
+                    }
                 }
             }
+            if (SPL > 1 && tr) trace_ev(p, TR_SPLIT, 2 * jt + 1);
             if constexpr (KIND != KIND_GEMM) {
                 // ---- store via TMA (bias + ReLU fused): per 16-channel block, the half's
                 // 128 threads write their pixel's 64 bytes into a SW64 smem image of the
@@ -1392,6 +1439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (KIND != KIND_GEMM && warp >= kEpiWarp0 && ((warp - kEpiWarp0) & 3) == 0 && lane == 0)
         bulk_wait<0>();  // output boxes written before the CTA retires
     __syncwarp();
+    if (threadIdx.x == kEpiWarp0 * 32) trace_ev(p, TR_KERNEL, 3);
     tc_fence_before();
     if (CL > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
     else __syncthreads();
@@ -1399,6 +1447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if constexpr (PAIR) tmem_dealloc2<L::TMEM_COLS>(tmem_base);
         else tmem_dealloc<L::TMEM_COLS>(tmem_base);
+        if (lane == 0) trace_ev(p, TR_KERNEL, 4);
     }
 }
 

@@ -46,6 +46,7 @@ _SMS = 148
 
 # include/pdl.h raster bits
 RASTER_M_FASTEST, RASTER_BOX_TILES, RASTER_SEG_TILES, RASTER_NO_HALO, RASTER_HALO_CG4 = 1, 2, 4, 16, 64
+RASTER_SINGLE_IMAGE_TILES = 8
 
 
 @dataclass(frozen=True, order=True)
@@ -59,6 +60,9 @@ class TileVariant:
     halo: str = "auto"    # "on" | "off" | "auto"
     seg: str = "auto"     # "on" | "off" | "auto"
     split: int = 0        # 0: library planner, 1: no split, k: k reduction ranges
+    tile: str = "auto"    # "auto": the library's box search over (pixels wide, pixels high, images);
+                          # "single": a tile holds several images only when a whole image fits;
+                          # "WxHxN": that box (PDL_RASTER_TILE)
 
     @property
     def cg(self) -> int:
@@ -66,11 +70,12 @@ class TileVariant:
 
     def provenance(self) -> dict:
         return {"bn": self.bn, "bk": self.bk, "cluster": self.cluster, "mode": self.mode,
-                "order": self.order, "halo": self.halo, "seg": self.seg, "split": self.split}
+                "order": self.order, "halo": self.halo, "seg": self.seg, "split": self.split,
+                "tile": self.tile}
 
 
 def make_variant(bn: int, bk: int, cluster: int, mode: str = "3xtf32", order: str = "n",
-                 halo: str = "auto", seg: str = "auto", split: int = 0) -> TileVariant:
+                 halo: str = "auto", seg: str = "auto", split: int = 0, tile: str = "auto") -> TileVariant:
     """Variant with its canonical id (defaults leave no suffix, so the ids of the
     round-1 bn x bk x cluster menu are unchanged)."""
     vid = f"bn{bn}_bk{bk}_c{cluster}_{mode}"
@@ -82,13 +87,16 @@ def make_variant(bn: int, bk: int, cluster: int, mode: str = "3xtf32", order: st
         vid += "_s1" if seg == "on" else "_s0"
     if split:
         vid += f"_k{split}"
-    return TileVariant(vid, bn, bk, cluster, mode, order, halo, seg, split)
+    if tile != "auto":
+        vid += "_t1" if tile == "single" else f"_t{tile}"
+    return TileVariant(vid, bn, bk, cluster, mode, order, halo, seg, split, tile)
 
 
 def variant_from_record(vid: str, rec: dict, mode: str) -> TileVariant:
     """Rebuild a variant from a sweep record (scripts/sweep_variants.py)."""
     return TileVariant(vid, rec["bn"], rec["bk"], rec["cluster"], mode, rec.get("order", "n"),
-                       rec.get("halo", "auto"), rec.get("seg", "auto"), rec.get("split", 0))
+                       rec.get("halo", "auto"), rec.get("seg", "auto"), rec.get("split", 0),
+                       rec.get("tile", "auto"))
 
 
 @dataclass
@@ -101,6 +109,7 @@ class VariantConfig:
     halo_menu: tuple = ("auto", "on", "off")
     seg_menu: tuple = ("auto", "on", "off")
     split_menu: tuple = (0, 1, 2, 3, 4, 6, 8)   # used only when the tiles leave SMs idle
+    tile_menu: tuple = ("auto", "single")
     cap: int = 256
 
 
@@ -123,10 +132,10 @@ def legal(layer, v: TileVariant) -> bool:
     if _is_gemm(layer):
         # GEMM instances: bn in {64, 128}, bk = 32, cluster in {1, 2, 4}
         return v.bk == 32 and v.bn in (64, 128) and v.cluster in (1, 2, 4) and \
-            not (v.bn > 64 and layer.N <= 64) and v.halo == "auto" and v.seg == "auto"
+            not (v.bn > 64 and layer.N <= 64) and v.halo == "auto" and v.seg == "auto" and v.tile == "auto"
     if _is_stem(layer):
         return v.bn == 64 and v.cluster == 1 and v.bk == 32 and v.order == "n" and \
-            v.halo == "auto" and v.seg == "auto" and v.split in (0, 1)
+            v.halo == "auto" and v.seg == "auto" and v.split in (0, 1) and v.tile == "auto"
     ct = (layer.C + 15) // 16
     if v.bn == 256:
         # TF32 instance only, whole 256-column slices, no cluster / split (conv_default_cfg)
@@ -174,6 +183,11 @@ def emit_launch(v: TileVariant) -> dict:
         raster |= RASTER_BOX_TILES
     elif v.seg == "on":
         raster |= RASTER_SEG_TILES
+    if v.tile == "single":
+        raster |= RASTER_SINGLE_IMAGE_TILES
+    elif v.tile != "auto":
+        bw, bh, bni = (int(t) for t in v.tile.split("x"))
+        raster |= bw << 8 | bh << 16 | bni << 24
     cfg = {"bm": 128, "bn": v.bn, "bk": v.bk, "cluster_m": v.cluster}
     if raster:
         cfg["raster"] = raster
@@ -282,15 +296,16 @@ def generate_variants(nest_or_layer, cfg: VariantConfig = VariantConfig(), bindi
                         for halo in (("auto",) if gemm or stem else cfg.halo_menu):
                             for seg in (("auto",) if gemm or stem else cfg.seg_menu):
                                 for sp in splits:
-                                    v = make_variant(bn, 16 * cg, cl, mode, order, halo, seg, sp)
-                                    if not legal(layer, v):
-                                        continue
-                                    try:
-                                        sig = _signature(schedule(layer, v, n), v)
-                                    except Exception:  # noqa: BLE001
-                                        continue
-                                    if sig not in seen or v.vid < seen[sig].vid:
-                                        seen[sig] = v
+                                    for tile in (("auto",) if gemm or stem else cfg.tile_menu):
+                                        v = make_variant(bn, 16 * cg, cl, mode, order, halo, seg, sp, tile)
+                                        if not legal(layer, v):
+                                            continue
+                                        try:
+                                            sig = _signature(schedule(layer, v, n), v)
+                                        except Exception:  # noqa: BLE001
+                                            continue
+                                        if sig not in seen or v.vid < seen[sig].vid:
+                                            seen[sig] = v
     vs = sorted(seen.values(), key=lambda v: v.vid)
     if not vs:
         import warnings

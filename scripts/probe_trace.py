@@ -6,8 +6,8 @@ import paper_2006_02230_b200 as P
 from paper_2006_02230_b200 import _lib, workloads as W
 L = _lib.lib()
 L.pdl_debug_set_trace.argtypes = [ctypes.c_void_p]
-N_EV, TN = 11, 4096
-names = ["P_ISSUE", "S_FULL", "S_TFREE", "S_DONE", "M_READY", "M_ISSUED", "E_FULL", "E_DRAINED", "E_STORED", "M_WAITED", "M_LOOP"]
+N_EV, TN = 13, 4096
+names = ["P_ISSUE", "S_FULL", "S_TFREE", "S_DONE", "M_READY", "M_ISSUED", "E_FULL", "E_DRAINED", "E_STORED", "M_WAITED", "M_LOOP", "KERNEL", "SPLIT"]
 out = {}
 import os
 CL = int(os.environ.get("CL", "0"))

@@ -260,10 +260,15 @@ def test_engine_geometry_matches_host_rules():
     L = workloads.ConvLayer(2, 64, 64, 56, 1, 1, 1)  # 1x1 s1 56x56: flattened to 3136 px rows
     g = V.engine_geometry(L, V.TileVariant("x", 64, 32, 1), 256)
     assert g["flat"] and g["bw"] == 128 and g["bh"] == 1 and g["m_tiles"] == 25 * 256
-    L3 = workloads.ConvLayer(18, 512, 512, 7, 3, 1, 1)  # 7x7: 2 images per tile (98 rows)
+    L3 = workloads.ConvLayer(18, 512, 512, 7, 3, 1, 1)  # 7x7 3x3: one row of 18 images per tile (126 rows)
     g = V.engine_geometry(L3, V.TileVariant("x", 128, 32, 1), 256)
-    assert (g["bw"], g["bh"], g["bni"], g["rows_valid"]) == (7, 7, 2, 98)
+    assert (g["bw"], g["bh"], g["bni"], g["rows_valid"], g["halo"]) == (7, 1, 18, 126, 0)
     assert g["num_kb"] == (512 // 32) * 9
+    # the round-1 geometry: whole images, 2 per tile (98 rows), halo mode
+    g = V.engine_geometry(L3, V.make_variant(128, 32, 1, tile="single"), 256)
+    assert (g["bw"], g["bh"], g["bni"], g["rows_valid"], g["halo"]) == (7, 7, 2, 98, 1)
+    g = V.engine_geometry(L3, V.make_variant(128, 32, 1, tile="7x2x9"), 256)
+    assert (g["bw"], g["bh"], g["bni"], g["rows_valid"]) == (7, 2, 9, 126)
 
 
 def test_b200_stats_and_model_rank():
