@@ -623,6 +623,10 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
     // (the 12 N=64 MMAs of a 32-channel block do not cover the pass overhead;
     // measured 0.39 -> 0.345 ms on ResNet layer 3, profiles/sweep_r1.json)
     if (c->bn == 64 && R * S > 1 && CT % 4 == 0) cg = 4;
+    // ... and BN=64 1x1 convs with >= 128 input channels (round-2 sweep, profiles/sweep_r2n_b256.json:
+    // ResNet layer 5, c256 -> k64: 0.196 ms against 0.224-0.235 ms with resident weights and
+    // 32-channel k-blocks; layer 2, c64 -> k64, would have one k-block per tile and keeps them)
+    if (c->bn == 64 && R * S == 1 && CT % 4 == 0 && CT >= 8 && (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32) cg = 4;
     // TF32: 64-channel k-blocks everywhere the channels allow (one weight plane per stage
     // leaves room).  A 32-channel TF32 k-block is 4 MMAs against the fixed per-k-block
     // hand-off; doubling it made the 1x1 layers 25-35% faster (layer 13: 122.8 -> 88.9 us,
