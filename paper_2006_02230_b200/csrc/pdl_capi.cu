@@ -237,6 +237,7 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
         if (bn == 128 && cg == 4 && (!SPLIT3 || CL == 1)) return launch_tile<KIND, 128, 4, SPLIT3, CL>(maps, p, work, s);
         if constexpr (!SPLIT3 && CL == 1) {
             if (bn == 256 && cg == 2) return launch_tile<KIND, 256, 2, false, 1>(maps, p, work, s);
+            if (bn == 256 && cg == 4) return launch_tile<KIND, 256, 4, false, 1>(maps, p, work, s);
         }
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
