@@ -459,9 +459,33 @@ struct BoxShape {
     int bw = 0, bh = 0, bni = 0;
     long long tiles = 0, waves = 0;
 };
+BoxShape pick_box_search(int N, int Pg, int Qg, int n_tiles, int halo_r, int halo_s, long long wave);
+
+// The search costs 5-15 us of host time; its result only depends on the arguments, so calls
+// repeat it from a table (eager launches of 20-us layers would otherwise wait for the host).
 BoxShape pick_box(int N, int Pg, int Qg, int n_tiles, int halo_r, int halo_s) {
+    struct Key {
+        int v[7];
+        bool operator<(const Key &o) const { return std::lexicographical_compare(v, v + 7, o.v, o.v + 7); }
+    };
+    static std::mutex mu;
+    static std::map<Key, BoxShape> table;
+    const int wave = sms();
+    const Key k{{N, Pg, Qg, n_tiles, halo_r, halo_s, wave}};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = table.find(k);
+        if (it != table.end()) return it->second;
+    }
+    const BoxShape b = pick_box_search(N, Pg, Qg, n_tiles, halo_r, halo_s, wave);
+    std::lock_guard<std::mutex> lock(mu);
+    if (table.size() > 4096) table.clear();
+    table[k] = b;
+    return b;
+}
+
+BoxShape pick_box_search(int N, int Pg, int Qg, int n_tiles, int halo_r, int halo_s, long long wave) {
     const int halo_px = pdl::kHaloSub / 64;
-    const long long wave = sms();
     BoxShape best;
     for (int pass = 0; pass < 2; ++pass) {
         // pass 0: the fewest waves (then tiles); pass 1: the widest box within the slack of it
@@ -640,15 +664,33 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
     // (its TS MMAs need TMEM columns the two 256-column accumulators use).  1x1 layers
     // 10-21% faster in the suite; 3x3 layers 12/17 151 -> 135 / 168 -> 132 us isolated.
     // (not when the caller asks for a multicast cluster or split-K, which 256 tiles lack)
+    // (round 2: 64-channel k-blocks for the spatial filters -- two 96 KB stages, 8 MMAs per k-block
+    // against the hand-off: layers 12 / 17 122 -> 114 / 155 -> 141 us; the 1x1 layers lose 0-10% with
+    // them, profiles/tf32_bn256_bk64_r2q.log)
     if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_TF32 && K % 256 == 0 && CT % 2 == 0) {
         c->bn = 256;
-        cg = 2;
+        cg = (R * S > 1 && CT % 4 == 0) ? 4 : 2;
     }
     c->bk = 16 * cg;
     c->stages = 0;
     c->cluster_m = kDefaultConvCluster;
     c->cluster_n = c->split_k = 1;
     c->raster = 0;
+}
+
+// The default schedule of a call: conv_default_cfg, except that 256-column tiles (which cannot
+// split the reduction) give way to the 128-column schedule when they would leave SMs idle --
+// small batches: ResNet layer 17 at 32 images is 28 tiles of 256 columns (TF32 82 -> 46 us).
+void conv_auto_cfg(int N, int C, int K, int H, int W, int R, int S, int stride, int pad, unsigned flags,
+                   const pdl_tile_cfg *cfg_in, pdl_tile_cfg *cfg) {
+    conv_default_cfg(C, K, R, S, cfg, flags, !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1)));
+    if (cfg->bn == 256 && !(cfg_in && (cfg_in->bn || cfg_in->bk))) {
+        const ConvGeom g0 = conv_geom(N, H, W, R, S, stride, pad, false, K / 256, false,
+                                      cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES));
+        // (only when the twice as many 128-column tiles still fit one wave: 112 tiles of 256 columns
+        // -- layers 18 / 19 at 32 images -- beat 224 of 128 in two waves by 6-15%)
+        if (2ll * g0.m_tiles * (K / 256) <= sms()) conv_default_cfg(C, K, R, S, cfg, flags, false);
+    }
 }
 
 // Output map of the TMA-stored epilogue: y [N][KT][Pg][Qg][16] in the tile
@@ -838,7 +880,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
         return fail(PDL_EUNSUPPORTED, "conv: unsupported raster bits 0x%x", cfg_in->raster & ~kRasterBits);
     const bool split = (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32;
     pdl_tile_cfg cfg;
-    conv_default_cfg(C, K, R, S, &cfg, flags, !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1)));
+    conv_auto_cfg(N, C, K, H, W, R, S, stride, pad, flags, cfg_in, &cfg);
     if (cfg_in) {
         if (cfg_in->bn) cfg.bn = cfg_in->bn;
         if (cfg_in->bk) cfg.bk = cfg_in->bk;
@@ -1639,7 +1681,13 @@ size_t pdl_workspace_bytes(int op, const int *dims, const pdl_tile_cfg *cfg) {
 int pdl_default_cfg(int op, const int *dims, pdl_tile_cfg *cfg) {
     if (!cfg || !dims) return fail(PDL_EINVAL, "default_cfg: null argument");
     if (op == PDL_OP_CONV2D) {
-        conv_default_cfg(dims[1], dims[2], dims[5], dims[6], cfg, (unsigned)dims[9]);
+        // dims = {N, C, K, H, W, R, S, stride, pad, flags}
+        if (dims[0] <= 0 || dims[3] <= 0 || dims[4] <= 0 || (dims[7] != 1 && dims[7] != 2) ||
+            dims[3] + 2 * dims[8] < dims[5] || dims[4] + 2 * dims[8] < dims[6])
+            conv_default_cfg(dims[1], dims[2], dims[5], dims[6], cfg, (unsigned)dims[9]);
+        else
+            conv_auto_cfg(dims[0], dims[1], dims[2], dims[3], dims[4], dims[5], dims[6], dims[7], dims[8],
+                          (unsigned)dims[9], nullptr, cfg);
         return PDL_OK;
     }
     if (op == PDL_OP_GEMM) {

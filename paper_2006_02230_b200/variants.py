@@ -139,7 +139,7 @@ def legal(layer, v: TileVariant) -> bool:
     ct = (layer.C + 15) // 16
     if v.bn == 256:
         # TF32 instance only, whole 256-column slices, no cluster / split (conv_default_cfg)
-        if not (v.mode == "tf32" and v.cg == 2 and v.cluster == 1 and layer.K % 256 == 0 and v.split in (0, 1)):
+        if not (v.mode == "tf32" and v.cg in (2, 4) and v.cluster == 1 and layer.K % 256 == 0 and v.split in (0, 1)):
             return False
     elif (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
         return False
