@@ -145,6 +145,30 @@ def fam_segtiles():
     return conv_case(256, 256, 14, 1, 1, 5, cfg={"raster": 4}, expect={"seg_rows": 9})
 
 
+def _tile(bw, bh, bni):
+    return {"raster": bw << 8 | bh << 16 | bni << 24}  # PDL_RASTER_TILE
+
+
+def fam_multibox_ragged():
+    # 7x1 pixels x 18 images per tile, 37 images: the last boxes hold images past N (TMA clips the stores)
+    return conv_case(256, 128, 14, 1, 2, 37, cfg=_tile(7, 1, 18), expect={"tile_w": 7, "tile_h": 1, "tile_images": 18})
+
+
+def fam_multibox_halo():
+    # 8x8 pixels x 2 images per tile with the halo path, odd batch
+    return conv_case(64, 64, 56, 3, 1, 5, cfg=_tile(8, 8, 2), expect={"tile_w": 8, "tile_h": 8, "tile_images": 2, "halo": 1})
+
+
+def fam_multibox_1x1():
+    # 7x7 1x1, rows of 18 images, 23 images
+    return conv_case(256, 256, 7, 1, 1, 23, cfg=_tile(7, 1, 18), expect={"tile_w": 7, "tile_images": 18, "flat": 0})
+
+
+def fam_multibox_splitk():
+    # 7x7 3x3 at a small batch: 7x1 x 18 images, per-tap boxes, two split-K ranges (register fast path)
+    return conv_case(512, 512, 7, 3, 1, 32, expect={"tile_images": 18, "split": 2})
+
+
 def fam_cluster():
     return conv_case(256, 256, 14, 1, 1, 4, cfg={"cluster_m": 2}, expect={"cluster": 2})
 

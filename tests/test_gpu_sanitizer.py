@@ -41,7 +41,8 @@ def test_family_oracle_canaries_and_repeat(cases, family):
     cases.FAMILIES[family]()
 
 
-@pytest.mark.parametrize("family", ["halo_splitk", "splitk", "gemm_splitk", "host", "segtiles", "stem"])
+@pytest.mark.parametrize("family", ["halo_splitk", "splitk", "gemm_splitk", "host", "segtiles", "stem", "multibox_ragged",
+                                    "multibox_splitk"])
 def test_family_many_launches_stable(cases, family):
     """20 back-to-back runs of the families with cross-launch state (self-resetting
     split-K counters, host-pipeline events, persistent tile rings)."""
