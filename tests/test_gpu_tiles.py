@@ -104,3 +104,44 @@ def test_explicit_tile_box(P, case, mode):
     assert rel(sp.cpu().numpy(), ref) <= (1e-5 if mode == "3xtf32" else 1e-2)
     sp2 = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 2, "raster": tile(*shape), "bn": min(128, s["bn"])}, **kw)
     assert torch.equal(sp, sp2), "split-K result depends on the arrival order"
+
+
+def _random_cases(n_cases=48, seed=2026):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n_cases:
+        R = int(rng.choice([1, 1, 3, 3, 5]))
+        S = int(rng.choice([R, R, 1 if R == 1 else 3]))
+        stride = int(rng.choice([1, 1, 2]))
+        pad_h = int(rng.choice([0, min(R, S) // 2]))
+        H, Wd = int(rng.integers(max(R, 2), 41)), int(rng.integers(max(S, 2), 41))
+        C = int(rng.choice([16, 32, 48, 64, 128]))
+        K = int(rng.choice([16, 32, 64, 128, 256]))
+        N = int(rng.integers(1, 41))
+        if pad_h >= R or pad_h >= S or H + 2 * pad_h < R or Wd + 2 * pad_h < S:
+            continue
+        if N * C * H * Wd > 6_000_000 or C * K * R * S > 1_500_000:
+            continue
+        out.append((C, K, H, Wd, R, S, stride, pad_h, N))
+    return out
+
+
+@pytest.mark.parametrize("case", _random_cases(), ids=lambda c: "c%dk%dh%dw%dr%ds%dst%dp%dn%d" % c)
+def test_random_shapes_box_search(P, case):
+    """Seeded random shapes (non-square maps and filters, pad 0 or 'same', ragged batches):
+    the box search, the round-1 geometry and the fp64 oracle agree -- the first two bitwise."""
+    C, K, H, Wd, R, S, stride, pad, N = case
+    rng = np.random.default_rng(hash(case) % (1 << 31))
+    x = rng.uniform(-1, 1, size=(N, C // 16, H, Wd, 16)).astype(np.float32)
+    w = rng.uniform(-1, 1, size=(K // 16, C // 16, R, S, 16, 16)).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, size=(K,)).astype(np.float32)
+    pw = P.prepack_weights(torch.from_numpy(w).cuda())
+    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    kw = dict(stride=stride, pad=pad, relu=True)
+    new = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 1}, **kw)
+    old = P.conv2d_nchw16c(xd, pw, bd, cfg={"split_k": 1, "raster": SINGLE}, **kw)
+    ref = oracle.conv2d_f64(x, w, b, stride=stride, pad=pad, relu=True)
+    assert rel(new.cpu().numpy(), ref) <= 1e-5
+    assert torch.equal(new, old), "the tile shape changed the per-element reduction"
+    auto = P.conv2d_nchw16c(xd, pw, bd, **kw)  # + split-K when it engages
+    assert rel(auto.cpu().numpy(), ref) <= 1e-5
