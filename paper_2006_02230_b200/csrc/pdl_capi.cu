@@ -239,6 +239,10 @@ int dispatch_bn(int bn, int cg, const pdl::TmaMaps &maps, const pdl::TileParams 
             if (bn == 256 && cg == 2) return launch_tile<KIND, 256, 2, false, 1>(maps, p, work, s);
             if (bn == 256 && cg == 4) return launch_tile<KIND, 256, 4, false, 1>(maps, p, work, s);
         }
+        if constexpr (SPLIT3 && CL == 1) {
+            // 3xTF32 at 256 columns: one accumulator, register-traded epilogue (see the kernel)
+            if (bn == 256 && cg == 2) return launch_tile<KIND, 256, 2, true, 1>(maps, p, work, s);
+        }
     }
     return fail(PDL_EUNSUPPORTED, "no kernel instance for bn=%d cg=%d cluster=%d", bn, cg, CL);
 }
@@ -683,7 +687,26 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
 // small batches: ResNet layer 17 at 32 images is 28 tiles of 256 columns (TF32 82 -> 46 us).
 void conv_auto_cfg(int N, int C, int K, int H, int W, int R, int S, int stride, int pad, unsigned flags,
                    const pdl_tile_cfg *cfg_in, pdl_tile_cfg *cfg) {
-    conv_default_cfg(C, K, R, S, cfg, flags, !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1)));
+    const bool wide = !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1));
+    conv_default_cfg(C, K, R, S, cfg, flags, wide);
+    // 3xTF32 at 256 columns (one accumulator, register-traded epilogue; results bitwise those of the
+    // 128-column tiles): half the A fill, staging and k-block hand-offs per flop, but two 80 KB stages
+    // and no accumulator double-buffering.  Measured (profiles/bn256_3xtf32_r2y.log) 3-9% faster on the
+    // 1x1 layers with >= 512 output channels when the tile count keeps the waves (layers 8 / 9 / 13 /
+    // 14 / 18 / 19), 11-36% slower with one 256-column N-tile (every A tile straight from HBM through
+    // two stages: layers 4 / 11 / 15) or when it costs a wave (layers 16 / 17 / 20).
+    if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 && !(flags & (PDL_SCALE | PDL_RELU6)) &&
+        cfg->bn == 128 && cfg->bk == 32 && R * S == 1 && K % 256 == 0 && K >= 512 &&
+        !(cfg_in && (cfg_in->bn || cfg_in->bk || cfg_in->cluster_n))) {
+        const bool single = cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES);
+        const ConvGeom g1 = conv_geom(N, H, W, R, S, stride, pad, false, K / 128, false, single);
+        const ConvGeom g2 = conv_geom(N, H, W, R, S, stride, pad, false, K / 256, false, single);
+        const long long wave = sms();
+        const long long t1 = (long long)g1.m_tiles * (K / 128), t2 = (long long)g2.m_tiles * (K / 256);
+        // (at least four waves of 256-column tiles: at 2-3 waves -- layers 8 / 9 at 28-32 images -- the
+        // two-stage pipeline's ramp costs more than the tiles save, 3-13% slower)
+        if (t2 >= 4 * wave && 2 * ((t2 + wave - 1) / wave) <= (t1 + wave - 1) / wave) cfg->bn = 256;
+    }
     if (cfg->bn == 256 && !(cfg_in && (cfg_in->bn || cfg_in->bk))) {
         const ConvGeom g0 = conv_geom(N, H, W, R, S, stride, pad, false, K / 256, false,
                                       cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES));
@@ -903,6 +926,7 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     // (loaded once per CTA; stages carry A only) unless a multicast cluster is asked for
     const int res_plane = ceil16(C) * 16 * cfg.bn * 4;
     const bool resident = split && !pair && !epix && R == 1 && S == 1 && cfg.bk == 32 && res_plane <= 65536 &&
+                          cfg.bn <= 128 &&
                           (!cfg_in || cfg_in->cluster_m <= 1);
     if (resident) cfg.cluster_m = 1;
     const int CT = ceil16(C), KT = K / 16, cg = cfg.bk / 16;
@@ -939,7 +963,8 @@ int conv_fwd_tc(const float *x, const float *wp, const float *bias, float *y, in
     const int m_tiles = g.m_tiles, n_tiles = (K + cfg.bn - 1) / cfg.bn;
     const int num_kb = (CT / cg) * R * S;
     // BN=256 (TF32): one accumulation segment per tile, never split (streaming epilogue)
-    const int seg_kb = cfg.bn > 128 ? num_kb : std::max(1, kSegElems / (16 * cg));
+    // BN=256: TF32 streams one accumulation segment per tile; 3xTF32 keeps the 256-element segments
+    const int seg_kb = (cfg.bn > 128 && !split) ? num_kb : std::max(1, kSegElems / (16 * cg));
     SplitPlan spl;
     spl.kb_per = num_kb;
     if (!pair && !resident && cfg.bn <= 128) {

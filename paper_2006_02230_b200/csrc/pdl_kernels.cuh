@@ -244,7 +244,10 @@ struct Smem {
     static constexpr int S0 = BUDGET / STAGE;
     static constexpr int STAGES = S0 > 16 ? 16 : S0;
     static constexpr int SLOT_COLS = SPLIT3 ? 2 * G::KS : G::KS;  // TMEM columns per A slot
-    static constexpr int A_SLOT0 = 2 * BN;                        // after the 2 accumulators
+    // 3xTF32 with 256 columns: ONE 256-column accumulator (two would fill TMEM and leave no A slots);
+    // the epilogue drains it at every segment end while the MMAs wait
+    static constexpr bool ONE_ACC = SPLIT3 && BN > 128;
+    static constexpr int A_SLOT0 = ONE_ACC ? BN : 2 * BN;         // after the accumulator(s)
     static constexpr int T0 = TS ? (512 - A_SLOT0) / SLOT_COLS : 1;
     static constexpr int TSLOTS = T0 > 8 ? 8 : T0;
     static constexpr int A_OFF = 0;
@@ -481,8 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(!PAIR || (CL == 2 && KIND == KIND_CONV && SPLIT3), "pairs: 3xTF32 conv, cluster 2");
     static_assert(!RESW || (KIND == KIND_CONV && CL == 1 && !PAIR && SPLIT3), "resident weights: 3xTF32 conv");
     static_assert(!HALO || (KIND == KIND_CONV && CL == 1 && !PAIR && !RESW), "halo: conv, cluster 1");
-    static_assert(BN <= 128 || (KIND == KIND_CONV && !SPLIT3 && !HALO && !RESW && CL == 1),
-                  "BN=256: TF32 conv, SS MMAs, cluster 1");
+    static_assert(BN <= 128 || (KIND == KIND_CONV && !HALO && !RESW && CL == 1 && !PAIR),
+                  "BN=256: conv, cluster 1");
     using G = Geo<KIND, BN, CG, PAIR>;
     using L = Smem<KIND, BN, CG, SPLIT3, PAIR, RESW, HALO>;
     constexpr bool TS = L::TS;
@@ -492,8 +495,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr bool FUSED = KIND == KIND_STEM && G::STEM_PACKED && SPLIT3;
     constexpr int PL = SPLIT3 ? 2 : 1;  // stem weight planes, layout [kb][chunk][plane][BN][4]
     // accumulator buffer / mbarrier parity of TMEM segment g
-    auto acc_buf = [](int g) { return FUSED ? 0 : (g & 1); };
-    auto acc_par = [](int g) { return (uint32_t)(FUSED ? (g & 1) : ((g >> 1) & 1)); };
+    constexpr bool ONE_ACC = FUSED || L::ONE_ACC;
+    // 3xTF32 at 256 columns: the epilogue threads sum 128 columns of segments in registers, past
+    // the 128 registers a 512-thread CTA gives each thread -- the warpgroups trade registers
+    // (setmaxnreg): warps 0-3 (TMA, MMA) 48, the staging warps 80, the epilogue warps 192
+    constexpr bool REGTRADE = L::ONE_ACC;
+    auto acc_buf = [](int g) { return ONE_ACC ? 0 : (g & 1); };
+    auto acc_par = [](int g) { return (uint32_t)(ONE_ACC ? (g & 1) : ((g >> 1) & 1)); };
     constexpr int TSLOTS = L::TSLOTS;
     constexpr int HALF = BN / 2;  // columns per epilogue warp
     extern __shared__ uint8_t smem_raw[];
@@ -590,7 +598,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) trace_ev(p, TR_KERNEL, 2);
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t smem0 = smem_u32(smem);
-
+    // REGTRADE: per-warpgroup register budgets (64 + 88 + 2 x 176 registers x 128 threads = 64 K), each
+    // set at the top of the warpgroup's own branch so that the code it dominates is allocated to it
+    if (warp < kSplitWarp0) {
+    if constexpr (REGTRADE) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
@@ -897,8 +908,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp >= kSplitWarp0 && warp < kEpiWarp0) {
+    }
+    } else if (warp < kEpiWarp0) {
         // ===================== A staging into TMEM (hi / lo) =====================
+        if constexpr (REGTRADE) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
         if constexpr (KIND == KIND_STEM) {
             // thread = output pixel (ph, pw) of the BW x BH tile; k-block = kernel row r:
             // gather taps 0..7 (4 channels each) of input row ph*stride + r from the
@@ -1117,8 +1130,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp >= kEpiWarp0) {
+    } else {
         // ===================== TMEM drain + epilogue =====================
+        if constexpr (REGTRADE) asm volatile("setmaxnreg.inc.sync.aligned.u32 176;");
         const int e = warp - kEpiWarp0;
         const int quarter = e & 3;
         const int half = e >> 2;
@@ -1132,7 +1146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kb0 = sp * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
             const int nseg = (kb1 - kb0 + seg_kb - 1) / seg_kb;
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
-            if constexpr (KIND == KIND_CONV && BN > 128) {
+            if constexpr (KIND == KIND_CONV && BN > 128 && !SPLIT3) {
                 // ---- streaming epilogue (TF32, BN=256: 128 columns per thread do not fit
                 // in registers): one segment per tile (the host sets seg_kb = num_kb, no
                 // split-K); each 16-column block goes TMEM -> registers -> smem box -> TMA

@@ -138,8 +138,9 @@ def legal(layer, v: TileVariant) -> bool:
             v.halo == "auto" and v.seg == "auto" and v.split in (0, 1) and v.tile == "auto"
     ct = (layer.C + 15) // 16
     if v.bn == 256:
-        # TF32 instance only, whole 256-column slices, no cluster / split (conv_default_cfg)
-        if not (v.mode == "tf32" and v.cg in (2, 4) and v.cluster == 1 and layer.K % 256 == 0 and v.split in (0, 1)):
+        # whole 256-column slices, no cluster / split; TF32: bk 32 / 64, 3xTF32: bk 32 (one accumulator)
+        if not (v.cg in ((2, 4) if v.mode == "tf32" else (2,)) and v.cluster == 1 and layer.K % 256 == 0 and
+                v.split in (0, 1)):
             return False
     elif (v.bn, v.cg) not in _CONV_INSTANCES and not (v.mode == "tf32" and (v.bn, v.cg) == (128, 4)):
         return False
@@ -165,7 +166,8 @@ def stage_sizes(v: TileVariant) -> dict:
     stages = min(16, _SMEM_BUDGET // stage)
     ks = 16 * v.cg
     slot = (2 * ks) if v.mode == "3xtf32" else ks
-    tslots = min(8, (512 - 2 * v.bn) // slot) if v.mode == "3xtf32" else 0
+    acc_cols = v.bn if v.bn > 128 else 2 * v.bn  # 3xTF32 at 256 columns: a single accumulator
+    tslots = min(8, (512 - acc_cols) // slot) if v.mode == "3xtf32" else 0
     return {"stage_bytes": stage, "stages": stages, "ks": ks, "tslots": tslots}
 
 
