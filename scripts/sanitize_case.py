@@ -169,6 +169,11 @@ def fam_multibox_splitk():
     return conv_case(512, 512, 7, 3, 1, 32, expect={"tile_images": 18, "split": 2})
 
 
+def fam_3xtf32_bn256():
+    # 256-column 3xTF32 tiles: single accumulator, register-traded epilogue, ragged batch and channels
+    return conv_case(256, 384, 14, 1, 1, 11, cfg={"bn": 256, "bk": 32}, expect={"bn": 256})
+
+
 def fam_cluster():
     return conv_case(256, 256, 14, 1, 1, 4, cfg={"cluster_m": 2}, expect={"cluster": 2})
 

@@ -145,3 +145,43 @@ def test_random_shapes_box_search(P, case):
     assert torch.equal(new, old), "the tile shape changed the per-element reduction"
     auto = P.conv2d_nchw16c(xd, pw, bd, **kw)  # + split-K when it engages
     assert rel(auto.cpu().numpy(), ref) <= 1e-5
+
+
+WIDE3 = [  # (C, K, H, R, stride, N)
+    (128, 512, 28, 1, 1, 5),
+    (256, 512, 56, 1, 2, 3),
+    (512, 1024, 14, 1, 1, 9),
+    (64, 256, 12, 3, 1, 4),     # 3x3 with per-tap boxes
+    (64, 384, 9, 1, 1, 7),      # K not a multiple of 256: the second N-tile is half empty
+    (1024, 256, 7, 1, 1, 37),   # 32 k-blocks = 4 accumulation segments through the single accumulator
+]
+
+
+@pytest.mark.parametrize("case", WIDE3, ids=lambda c: "c%dk%dh%dr%ds%dn%d" % c)
+def test_3xtf32_256_column_tiles(P, case):
+    """3xTF32 at 256 columns (one TMEM accumulator drained per segment, setmaxnreg register
+    trade): same segments and per-element order as the 128-column tiles, so bitwise equal to
+    them, and within 1e-5 of the oracle."""
+    C, K, H, R, stride, N = case
+    layer = W.ConvLayer(0, C, K, H, R, stride)
+    x, w, b = W.conv_inputs(layer, N, seed=41)
+    pw = P.prepack_weights(torch.from_numpy(w).cuda())
+    xd, bd = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    kw = dict(stride=stride, pad=R // 2, relu=True)
+    s = _lib.conv_schedule(N, C, K, H, H, R, R, stride, R // 2, 0, cfg={"bn": 256, "bk": 32})
+    assert s["bn"] == 256 and s["resident"] == 0 and s["split"] == 1
+    wide = P.conv2d_nchw16c(xd, pw, bd, cfg={"bn": 256, "bk": 32}, **kw)
+    narrow = P.conv2d_nchw16c(xd, pw, bd, cfg={"bn": 128, "bk": 32, "split_k": 1}, **kw)
+    ref = oracle.conv2d_f64(x, w, b, stride=stride, pad=R // 2, relu=True)
+    assert rel(wide.cpu().numpy(), ref) <= 1e-5
+    assert torch.equal(wide, narrow)
+    assert torch.equal(wide, P.conv2d_nchw16c(xd, pw, bd, cfg={"bn": 256, "bk": 32}, **kw))
+
+
+def test_3xtf32_256_columns_chosen_for_large_1x1_layers():
+    """Host-only: the default takes 256-column tiles for 1x1 convs with >= 512 output channels
+    at >= 4 waves, and never for small batches."""
+    picks = {n: [l.idx for l in W.LAYERS
+                 if _lib.conv_schedule(n, l.C, l.K, l.H, l.W, l.R, l.S, l.stride, l.pad, 0)["bn"] == 256]
+             for n in (256, 32)}
+    assert picks[256] == [8, 9, 13, 14, 18, 19] and picks[32] == []
