@@ -85,8 +85,6 @@ struct TileParams {
     int n_tiles;           // number of N tiles
     int raster;            // bit 0: M-tiles fastest tile order (see tile_coord)
     int seg_kb;            // k-blocks per TMEM accumulation segment
-    int pf;                // 1x1 conv: L2-prefetch the A boxes of the unit this many of the CTA's
-                           // units ahead (0: off) -- see the producer
     // split-K: every tile's reduction is cut into `split` ranges of kb_per k-blocks,
     // computed as separate work units; each writes its fp32 partial to part, and the
     // last of a tile's units to arrive (ctr[tile], self-resetting) sums the partials in
@@ -113,7 +111,8 @@ enum TraceEv {
     TR_M_WAITED,      // MMA: barrier observed (before tcgen05.fence::after_thread_sync)
     TR_M_LOOP,        // MMA: top of k-block loop
     TR_KERNEL,        // [0] kernel entry, [1] prologue done (barriers, TMEM), [2] after griddepcontrol.wait,
-                      // [3] before the final CTA sync (warp 8 lane 0), [4] after TMEM dealloc
+                      // [3] before the final CTA sync (warp 8 lane 0), [4] after TMEM dealloc, [5] producer entered,
+                      // [6] its first tile decoded, [7] before its first stage wait
     TR_SPLIT,         // split-K, per unit j: [2j] partial written + counter bumped, [2j+1] reduction read back
     TR_COUNT
 };
@@ -605,6 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
+            trace_ev(p, TR_KERNEL, 5);
             uint32_t tx;
             if (KIND == KIND_GEMM) tx = (uint32_t)(G::BM * 32 * 4 + BN * 32 * 4);
             else if (KIND == KIND_CONV)
@@ -659,31 +659,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int st = u / SPL;
                 const int kb0 = (u - st * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
                 const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
-                // L2 prefetch distance (1x1 convs on box tiles): the smem stages hold 1-3 tiles of
-                // A, less than the load latency once the layer's output stores fill the memory
-                // queues (traces: 5-13k cycles issue -> landed on ResNet layers 8 / 4, the MMAs
-                // starved 60-75% of the time).  The A boxes of the unit p.pf units ahead are
-                // prefetched into L2 k-block by k-block alongside this unit's loads.
-                bool pf_on = false;
-                TileCoord pfc = tc;
-                int pf_kb0 = 0, pf_kb1 = 0;
-                if (KIND == KIND_CONV && !HALO && p.pf > 0 && !p.seg_mode) {
-                    const int up = u + p.pf * ncl;
-                    if (up < num_units) {
-                        const int stp = up / SPL;
-                        pf_kb0 = (up - stp * SPL) * p.kb_per;
-                        pf_kb1 = min(p.num_kb, pf_kb0 + p.kb_per);
-                        pfc = tile_coord<KIND, BN>(p, tile_of(stp));
-                        pf_on = true;
-                    }
-                }
+                if (u == cid) trace_ev(p, TR_KERNEL, 6);
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
-                    if (KIND == KIND_CONV && !HALO && pf_on && pf_kb0 + (kb - kb0) < pf_kb1) {
-                        const int ctgp = pf_kb0 + (kb - kb0);  // R*S == 1: k-block = channel group
-#pragma unroll
-                        for (int c = 0; c < CG; ++c)
-                            tma_prefetch_5d(&maps.a[0], 0, pfc.q0, pfc.p0, ctgp * CG + c, pfc.i0);
-                    }
                     if constexpr (HALO) {
                         // new channel group (or the first k-block of this unit): its halo
                         const int rs_n = p.R * p.S;
@@ -699,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (++hb == L::HALO_NBUF) { hb = 0; hph ^= 1; }
                         }
                     }
+                    if (kglob == 0) trace_ev(p, TR_KERNEL, 7);
                     mbar_wait(&empty[s], ph ^ 1);
                     trace_ev(p, TR_P_ISSUE, kglob);
                     uint8_t *sp = smem + s * L::STAGE;

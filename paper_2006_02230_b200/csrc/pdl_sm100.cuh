@@ -81,15 +81,6 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *m, uin
         : "memory");
 }
 
-// L2 prefetch of a box (no shared-memory destination, no barrier): the producer issues it
-// for tiles further ahead than its smem stages reach, so the later TMA load hits L2.
-__device__ __forceinline__ void tma_prefetch_5d(const CUtensorMap *m, int c0, int c1, int c2, int c3, int c4) {
-    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
-                     reinterpret_cast<uint64_t>(m)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-                 : "memory");
-}
-
 // Multicast variants: the box lands at the same smem offset in every CTA of
 // `mask` and completes `bytes` on each destination CTA's mbarrier (same offset).
 __device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, uint64_t *bar,

@@ -49,7 +49,8 @@ for arg in sys.argv[2:]:
         return rel(v.min()) if len(v) else -1
     nkb = int((ev["M_ISSUED"] > 0).sum())
     print(f"{name}: event-timed {e0.elapsed_time(e1)*1e3:.1f} us (cold L2); block 0 cycles from kernel entry:")
-    print(f"   prologue done {rel(ev['KERNEL'][1])}, griddep wait done {rel(ev['KERNEL'][2])}, first TMA issue {first('P_ISSUE')}, "
+    print(f"   prologue done {rel(ev['KERNEL'][1])}, griddep wait done {rel(ev['KERNEL'][2])}, producer: entered {rel(ev['KERNEL'][5])} / "
+          f"first tile decoded {rel(ev['KERNEL'][6])} / before first stage wait {rel(ev['KERNEL'][7])}, first TMA issue {first('P_ISSUE')}, "
           f"first stage landed {first('S_FULL')}, first MMA ready {first('M_READY')}, last MMA issued {last('M_ISSUED')} ({nkb} k-blocks), "
           f"first acc full {first('E_FULL')}, last drained {last('E_DRAINED')}, split bumped {first('SPLIT')}..{last('SPLIT')}, "
           f"last stored {last('E_STORED')}, epilogue exit {rel(ev['KERNEL'][3])}, dealloc {rel(ev['KERNEL'][4])}", flush=True)
