@@ -574,16 +574,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (PAIR) tmem_alloc2<L::TMEM_COLS>(tmem_slot);
         else tmem_alloc<L::TMEM_COLS>(tmem_slot);
     }
-    if (warp == 3) {
-        // the otherwise idle warp touches every word of the geometry parameters, so the
-        // constant-bank lines the producer's first tile_coord needs are resident when the
-        // prologue ends (timelines of short launches: 2200 cycles from the end of the
-        // prologue to the first TMA issue, mostly a chain of constant-cache misses)
-        const unsigned *pw = reinterpret_cast<const unsigned *>(&p);
-        unsigned acc = 0;
-        for (int i = lane; i < (int)(sizeof(TileParams) / 4); i += 32) acc += pw[i];
-        asm volatile("" ::"r"(acc));
-    }
     tc_fence_before();
     if (CL > 1) cluster_sync();  // peers multicast into our barriers: they must exist
     else __syncthreads();
