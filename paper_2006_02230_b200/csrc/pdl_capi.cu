@@ -713,6 +713,17 @@ void conv_auto_cfg(int N, int C, int K, int H, int W, int R, int S, int stride, 
         // (only when the twice as many 128-column tiles still fit one wave: 112 tiles of 256 columns
         // -- layers 18 / 19 at 32 images -- beat 224 of 128 in two waves by 6-15%)
         if (2ll * g0.m_tiles * (K / 256) <= sms()) conv_default_cfg(C, K, R, S, cfg, flags, false);
+        else if (R * S > 1) {
+            // spatial filters: also when the 256-column tiling costs wave time (layer 17 at 256 images:
+            // 210 tiles = 2 waves against 420 half-size tiles in 3; TF32 142 -> 125 us,
+            // profiles/tf32_128v256_r2z.log; the 1x1 layers 16 / 20 tie, the rest prefer 256 columns)
+            const ConvGeom g1 = conv_geom(N, H, W, R, S, stride, pad, false, K / 128, false,
+                                          cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES));
+            const long long wave = sms();
+            const long long w2 = ((long long)g0.m_tiles * (K / 256) + wave - 1) / wave;
+            const long long w1 = ((long long)g1.m_tiles * (K / 128) + wave - 1) / wave;
+            if (2 * w2 > w1) conv_default_cfg(C, K, R, S, cfg, flags, false);
+        }
     }
 }
 
