@@ -570,6 +570,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_mbar_init();
     }
+    // The producer decodes its first unit here, while warp 2 allocates TMEM and the CTA syncs
+    // (timelines of short launches: ~0.7 us between the end of the prologue and the first TMA
+    // issue went into this decode)
+    TileCoord tc_first = {};
+    if (warp == 0 && lane == 0 && KIND != KIND_STEM && cid < num_units)
+        tc_first = tile_coord<KIND, BN>(p, tile_of(cid / SPL));
     if (warp == 2) {
         if constexpr (PAIR) tmem_alloc2<L::TMEM_COLS>(tmem_slot);
         else tmem_alloc<L::TMEM_COLS>(tmem_slot);
@@ -648,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = cid; KIND != KIND_STEM && u < num_units; u += ncl) {
                 const int st = u / SPL;
                 const int kb0 = (u - st * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
-                const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st));
+                const TileCoord tc = u == cid ? tc_first : tile_coord<KIND, BN>(p, tile_of(st));
                 if (u == cid) trace_ev(p, TR_KERNEL, 6);
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
                     if constexpr (HALO) {
