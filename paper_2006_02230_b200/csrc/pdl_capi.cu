@@ -210,6 +210,14 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
         pt.split = 1;
         pt.kb_per = pt.num_kb;
     }
+    pt.fd_n_tiles = pdl::make_fastdiv(pt.n_tiles);
+    pt.fd_m_tiles = pdl::make_fastdiv(pt.m_tiles);
+    pt.fd_tiles_w = pdl::make_fastdiv(pt.tiles_w);
+    pt.fd_tiles_h = pdl::make_fastdiv(pt.tiles_h);
+    pt.fd_split = pdl::make_fastdiv(pt.split);
+    pt.fd_P = pdl::make_fastdiv(pt.P);
+    pt.fd_rs = pdl::make_fastdiv(pt.R * pt.S);
+    pt.fd_S = pdl::make_fastdiv(pt.S);
     cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, pt);
     if (e != cudaSuccess) return fail(PDL_ELAUNCH, "tile_mma_kernel launch: %s", cudaGetErrorString(e));
     ++g_launches;

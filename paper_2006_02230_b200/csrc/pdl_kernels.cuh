@@ -55,6 +55,29 @@ constexpr unsigned kDiagBits = 0x1f00u;
 #define PDL_DBG(p, bit) false
 #endif
 
+// Division by a runtime constant without the ~100-cycle integer divide: q = umulhi(x, mul) >> shr
+// (mul = ceil(2^(31 + ceil(log2 d)) / d); exact for 0 <= x < 2^31).  The tile decode of every role
+// divides by the tile-grid extents once per work unit; with hardware divides one decode is ~700
+// cycles, on the critical path of short tiles' epilogues.
+struct FastDiv {
+    unsigned mul, shr;
+    int d;
+};
+inline FastDiv make_fastdiv(int d) {
+    FastDiv f{0u, 0u, d > 0 ? d : 1};
+    if (f.d > 1) {
+        unsigned a = 0;
+        while ((1u << a) < (unsigned)f.d) ++a;  // ceil(log2 d)
+        const unsigned p = 31 + a;
+        f.mul = (unsigned)(((1ull << p) + (unsigned)f.d - 1) / (unsigned)f.d);
+        f.shr = p - 32;
+    }
+    return f;
+}
+__device__ __forceinline__ int fdiv(int x, const FastDiv &f) {
+    return f.d == 1 ? x : (int)(__umulhi((unsigned)x, f.mul) >> f.shr);
+}
+
 // Geometry / epilogue parameters (by value, param space).
 struct TileParams {
     // common
@@ -93,6 +116,8 @@ struct TileParams {
     float *part;
     int *ctr;
     unsigned long long *trace;  // PDL_TRACE builds: per-event clock64 stamps of block 0
+    // divisors of the tile decode (filled by launch_tile from the fields above)
+    FastDiv fd_n_tiles, fd_m_tiles, fd_tiles_w, fd_tiles_h, fd_split, fd_P, fd_rs, fd_S;
 };
 
 // Timeline tracing (PDL_TRACE builds only): block 0 stamps clock64 at each
@@ -410,10 +435,10 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     // the stem, resident-weight tiles and clusters (one N-tile per CTA / cluster lockstep).
     int mt, nt;
     if (p.raster & 1) {
-        nt = tile / p.m_tiles;
+        nt = fdiv(tile, p.fd_m_tiles);
         mt = tile - nt * p.m_tiles;
     } else {
-        mt = tile / p.n_tiles;
+        mt = fdiv(tile, p.fd_n_tiles);
         nt = tile - mt * p.n_tiles;
     }
     c.n0 = nt * BN;
@@ -426,14 +451,14 @@ __device__ __forceinline__ TileCoord tile_coord(const TileParams &p, int tile) {
     } else if (p.seg_mode) {
         // segment tiles: bands [mt * seg_tile, +seg_tile); i0 = image group, p0 = first row
         const int g0 = mt * p.seg_tile;
-        c.i0 = g0 / p.P;
+        c.i0 = fdiv(g0, p.fd_P);
         c.p0 = g0 - c.i0 * p.P;
     } else {
         int t = mt;
-        const int tw = t % p.tiles_w;
-        t /= p.tiles_w;
-        const int th = t % p.tiles_h;
-        t /= p.tiles_h;
+        const int t1 = fdiv(t, p.fd_tiles_w);
+        const int tw = t - t1 * p.tiles_w;
+        t = fdiv(t1, p.fd_tiles_h);
+        const int th = t1 - t * p.tiles_h;
         c.q0 = tw * p.BW;
         c.p0 = th * p.BH;
         c.i0 = t * p.BNI;
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_units = num_super * SPL;   // work unit u = (super-tile u / SPL, split u % SPL)
     const uint16_t cl_mask = (uint16_t)((1u << CL) - 1);
     auto tile_of = [&](int st) {  // M-tile may exceed m_tiles (phantom: loads OOB zeros, stores masked)
-        const int mg = st / p.n_tiles;
+        const int mg = fdiv(st, p.fd_n_tiles);
         const int nt = st - mg * p.n_tiles;
         return (mg * CL + rank) * p.n_tiles + nt;
     };
@@ -575,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // issue went into this decode)
     TileCoord tc_first = {};
     if (warp == 0 && lane == 0 && KIND != KIND_STEM && cid < num_units)
-        tc_first = tile_coord<KIND, BN>(p, tile_of(cid / SPL));
+        tc_first = tile_coord<KIND, BN>(p, tile_of(fdiv(cid, p.fd_split)));
     if (warp == 2) {
         if constexpr (PAIR) tmem_alloc2<L::TMEM_COLS>(tmem_slot);
         else tmem_alloc<L::TMEM_COLS>(tmem_slot);
@@ -652,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             for (int u = cid; KIND != KIND_STEM && u < num_units; u += ncl) {
-                const int st = u / SPL;
+                const int st = fdiv(u, p.fd_split);
                 const int kb0 = (u - st * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
                 const TileCoord tc = u == cid ? tc_first : tile_coord<KIND, BN>(p, tile_of(st));
                 if (u == cid) trace_ev(p, TR_KERNEL, 6);
@@ -660,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (HALO) {
                         // new channel group (or the first k-block of this unit): its halo
                         const int rs_n = p.R * p.S;
-                        const int ctg = kb / rs_n;
+                        const int ctg = fdiv(kb, p.fd_rs);
                         if (kb - ctg * rs_n == 0 || kb == kb0) {
                             mbar_wait(&hempty[hb], hph ^ 1);
                             mbar_arrive_expect_tx(&hfull[hb], htx);
@@ -689,9 +714,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     } else if (KIND == KIND_CONV) {
                         const int rs_n = p.R * p.S;
-                        const int ctg = kb / rs_n;
+                        const int ctg = fdiv(kb, p.fd_rs);
                         const int rs = kb - ctg * rs_n;
-                        const int r = rs / p.S;
+                        const int r = fdiv(rs, p.fd_S);
                         const int sx = rs - r * p.S;
                         int dh = r - p.pad, dw = sx - p.pad, mi = 0;
                         if (p.stride == 2) {
@@ -757,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int num_kb = p.num_kb;
             // pairs: only the leader CTA issues (its MMAs drive both CTAs' tensor cores)
             for (int u = cid; u < num_units && (!PAIR || rank == 0); u += ncl) {
-                const int kb0 = (u - (u / SPL) * SPL) * p.kb_per, kb1 = min(num_kb, kb0 + p.kb_per);
+                const int kb0 = (u - fdiv(u, p.fd_split) * SPL) * p.kb_per, kb1 = min(num_kb, kb0 + p.kb_per);
                 int in_seg = 0;
                 uint32_t d_tmem = tmem_base;
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
@@ -1006,7 +1031,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             for (int u = cid; u < num_units; u += ncl) {
-                const int kb0 = (u - (u / SPL) * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
+                const int kb0 = (u - fdiv(u, p.fd_split) * SPL) * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
                 for (int kb = kb0; kb < kb1; ++kb, ++kglob) {
                     int hrow = 0;
                     bool group_end = false;
@@ -1015,9 +1040,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&full[s], ph);
                     if constexpr (HALO) {
                         const int rs_n = p.R * p.S;
-                        const int rs = kb - (kb / rs_n) * rs_n;
+                        const int rs = kb - fdiv(kb, p.fd_rs) * rs_n;
                         if (rs == 0 || kb == kb0) mbar_wait(&hfull[hb], hph);
-                        const int r = rs / p.S;
+                        const int r = fdiv(rs, p.fd_S);
                         hrow = hrow0 + r * p.box_w + (rs - r * p.S);
                         group_end = rs == rs_n - 1 || kb + 1 == kb1;
                     }
@@ -1116,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int g = 0, jt = 0;
         uint32_t eblk = 0;  // output boxes issued by this half (epilogue buffer ring)
         for (int u = cid; u < num_units; u += ncl, ++jt) {
-            const int st_i = u / SPL, sp = u - st_i * SPL;
+            const int st_i = fdiv(u, p.fd_split), sp = u - st_i * SPL;
             const int kb0 = sp * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
             const int nseg = (kb1 - kb0 + seg_kb - 1) / seg_kb;
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
