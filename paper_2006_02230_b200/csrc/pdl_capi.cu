@@ -218,6 +218,7 @@ int launch_tile(const pdl::TmaMaps &maps, const pdl::TileParams &p, int work_cta
     pt.fd_P = pdl::make_fastdiv(pt.P);
     pt.fd_rs = pdl::make_fastdiv(pt.R * pt.S);
     pt.fd_S = pdl::make_fastdiv(pt.S);
+    pt.fd_seg = pdl::make_fastdiv(pt.seg_kb);
     cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, pt);
     if (e != cudaSuccess) return fail(PDL_ELAUNCH, "tile_mma_kernel launch: %s", cudaGetErrorString(e));
     ++g_launches;

@@ -117,7 +117,7 @@ struct TileParams {
     int *ctr;
     unsigned long long *trace;  // PDL_TRACE builds: per-event clock64 stamps of block 0
     // divisors of the tile decode (filled by launch_tile from the fields above)
-    FastDiv fd_n_tiles, fd_m_tiles, fd_tiles_w, fd_tiles_h, fd_split, fd_P, fd_rs, fd_S;
+    FastDiv fd_n_tiles, fd_m_tiles, fd_tiles_w, fd_tiles_h, fd_split, fd_P, fd_rs, fd_S, fd_seg;
 };
 
 // Timeline tracing (PDL_TRACE builds only): block 0 stamps clock64 at each
@@ -1143,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = cid; u < num_units; u += ncl, ++jt) {
             const int st_i = fdiv(u, p.fd_split), sp = u - st_i * SPL;
             const int kb0 = sp * p.kb_per, kb1 = min(p.num_kb, kb0 + p.kb_per);
-            const int nseg = (kb1 - kb0 + seg_kb - 1) / seg_kb;
+            const int nseg = fdiv(kb1 - kb0 + seg_kb - 1, p.fd_seg);
             const TileCoord tc = tile_coord<KIND, BN>(p, tile_of(st_i));
             if constexpr (KIND == KIND_CONV && BN > 128 && !SPLIT3) {
                 // ---- streaming epilogue (TF32, BN=256: 128 columns per thread do not fit
