@@ -677,12 +677,12 @@ void conv_default_cfg(int C, int K, int R, int S, pdl_tile_cfg *c, unsigned flag
     // (its TS MMAs need TMEM columns the two 256-column accumulators use).  1x1 layers
     // 10-21% faster in the suite; 3x3 layers 12/17 151 -> 135 / 168 -> 132 us isolated.
     // (not when the caller asks for a multicast cluster or split-K, which 256 tiles lack)
-    // (round 2: 64-channel k-blocks for the spatial filters -- two 96 KB stages, 8 MMAs per k-block
-    // against the hand-off: layers 12 / 17 122 -> 114 / 155 -> 141 us; the 1x1 layers lose 0-10% with
-    // them, profiles/tf32_bn256_bk64_r2q.log)
+    // (64-channel k-blocks at 256 columns -- two 96 KB stages -- helped the spatial layers 12 / 17 by
+    // 6-8% while the tile decode still divided (profiles/tf32_bn256_bk64_r2q.log); with the divide-free
+    // decode 32-channel k-blocks win again, layer 12: 96 vs 117 us, profiles/sweep_r2z_b256.json)
     if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_TF32 && K % 256 == 0 && CT % 2 == 0) {
         c->bn = 256;
-        cg = (R * S > 1 && CT % 4 == 0) ? 4 : 2;
+        cg = 2;
     }
     c->bk = 16 * cg;
     c->stages = 0;
@@ -699,40 +699,17 @@ void conv_auto_cfg(int N, int C, int K, int H, int W, int R, int S, int stride, 
     const bool wide = !(cfg_in && (cfg_in->cluster_m > 1 || cfg_in->split_k > 1));
     conv_default_cfg(C, K, R, S, cfg, flags, wide);
     // 3xTF32 at 256 columns (one accumulator, register-traded epilogue; results bitwise those of the
-    // 128-column tiles): half the A fill, staging and k-block hand-offs per flop, but two 80 KB stages
-    // and no accumulator double-buffering.  Measured (profiles/bn256_3xtf32_r2y.log) 3-9% faster on the
-    // 1x1 layers with >= 512 output channels when the tile count keeps the waves (layers 8 / 9 / 13 /
-    // 14 / 18 / 19), 11-36% slower with one 256-column N-tile (every A tile straight from HBM through
-    // two stages: layers 4 / 11 / 15) or when it costs a wave (layers 16 / 17 / 20).
-    if (wide && (flags & PDL_MODE_MASK) == PDL_MODE_3XTF32 && !(flags & (PDL_SCALE | PDL_RELU6)) &&
-        cfg->bn == 128 && cfg->bk == 32 && R * S == 1 && K % 256 == 0 && K >= 512 &&
-        !(cfg_in && (cfg_in->bn || cfg_in->bk || cfg_in->cluster_n))) {
-        const bool single = cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES);
-        const ConvGeom g1 = conv_geom(N, H, W, R, S, stride, pad, false, K / 128, false, single);
-        const ConvGeom g2 = conv_geom(N, H, W, R, S, stride, pad, false, K / 256, false, single);
-        const long long wave = sms();
-        const long long t1 = (long long)g1.m_tiles * (K / 128), t2 = (long long)g2.m_tiles * (K / 256);
-        // (at least four waves of 256-column tiles: at 2-3 waves -- layers 8 / 9 at 28-32 images -- the
-        // two-stage pipeline's ramp costs more than the tiles save, 3-13% slower)
-        if (t2 >= 4 * wave && 2 * ((t2 + wave - 1) / wave) <= (t1 + wave - 1) / wave) cfg->bn = 256;
-    }
+    // 128-column tiles; cfg bn = 256, bk = 32) is NOT a default.  Before the tile decode lost its integer
+    // divides it was 3-9% faster on the 1x1 layers with >= 512 output channels (half as many tile
+    // decodes per flop: profiles/bn256_3xtf32_r2y.log); with the divide-free decode the 128-column
+    // tiles win by 5-10% on layers 9 / 14 / 18 / 19 and tie on 8 / 13 (profiles/bn256_vs_128_r2z.log):
+    // two 80 KB stages and an un-overlapped accumulator drain against four stages and two accumulators.
     if (cfg->bn == 256 && !(cfg_in && (cfg_in->bn || cfg_in->bk))) {
         const ConvGeom g0 = conv_geom(N, H, W, R, S, stride, pad, false, K / 256, false,
                                       cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES));
         // (only when the twice as many 128-column tiles still fit one wave: 112 tiles of 256 columns
         // -- layers 18 / 19 at 32 images -- beat 224 of 128 in two waves by 6-15%)
         if (2ll * g0.m_tiles * (K / 256) <= sms()) conv_default_cfg(C, K, R, S, cfg, flags, false);
-        else if (R * S > 1) {
-            // spatial filters: also when the 256-column tiling costs wave time (layer 17 at 256 images:
-            // 210 tiles = 2 waves against 420 half-size tiles in 3; TF32 142 -> 125 us,
-            // profiles/tf32_128v256_r2z.log; the 1x1 layers 16 / 20 tie, the rest prefer 256 columns)
-            const ConvGeom g1 = conv_geom(N, H, W, R, S, stride, pad, false, K / 128, false,
-                                          cfg_in && (cfg_in->raster & PDL_RASTER_SINGLE_IMAGE_TILES));
-            const long long wave = sms();
-            const long long w2 = ((long long)g0.m_tiles * (K / 256) + wave - 1) / wave;
-            const long long w1 = ((long long)g1.m_tiles * (K / 128) + wave - 1) / wave;
-            if (2 * w2 > w1) conv_default_cfg(C, K, R, S, cfg, flags, false);
-        }
     }
 }
 

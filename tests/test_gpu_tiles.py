@@ -178,10 +178,11 @@ def test_3xtf32_256_column_tiles(P, case):
     assert torch.equal(wide, P.conv2d_nchw16c(xd, pw, bd, cfg={"bn": 256, "bk": 32}, **kw))
 
 
-def test_3xtf32_256_columns_chosen_for_large_1x1_layers():
-    """Host-only: the default takes 256-column tiles for 1x1 convs with >= 512 output channels
-    at >= 4 waves, and never for small batches."""
-    picks = {n: [l.idx for l in W.LAYERS
-                 if _lib.conv_schedule(n, l.C, l.K, l.H, l.W, l.R, l.S, l.stride, l.pad, 0)["bn"] == 256]
-             for n in (256, 32)}
-    assert picks[256] == [8, 9, 13, 14, 18, 19] and picks[32] == []
+def test_3xtf32_256_columns_are_opt_in():
+    """Host-only: 256-column 3xTF32 tiles are only taken when asked for (cfg bn=256, bk=32)."""
+    for n in (256, 32):
+        for l in W.LAYERS:
+            assert _lib.conv_schedule(n, l.C, l.K, l.H, l.W, l.R, l.S, l.stride, l.pad, 0)["bn"] <= 128
+    l = W.LAYERS[18]
+    s = _lib.conv_schedule(256, l.C, l.K, l.H, l.W, l.R, l.S, l.stride, l.pad, 0, cfg={"bn": 256, "bk": 32})
+    assert s["bn"] == 256 and s["n_tiles"] == l.K // 256
