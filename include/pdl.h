@@ -52,7 +52,8 @@ extern "C" {
  * NULL or zero fields = library default.  bm is fixed at 128 (tcgen05 M). */
 typedef struct pdl_tile_cfg {
     int bm;        /* output rows (pixels / GEMM M) per CTA tile: 128          */
-    int bn;        /* output columns (K channels / GEMM N) per tile: 64|128     */
+    int bn;        /* output columns (K channels / GEMM N) per tile: 64|128, conv also 256
+                      (TF32 default for K % 256 == 0; 3xTF32 with bk = 32, opt-in)           */
     int bk;        /* reduction elements per pipeline stage (16*cg for conv)    */
     int stages;    /* smem pipeline depth                                       */
     int cluster_m; /* CTAs per cluster sharing (TMA-multicasting) a weight tile: 1|2|4 */
